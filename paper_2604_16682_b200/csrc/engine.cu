@@ -1,0 +1,276 @@
+/*
+ * engine.cu — sm_100a kernels behind the C ABI (include/agentsim_b200.h).
+ *
+ *   asb_engine_kernel : persistent, one warp per scenario, dynamic scenario
+ *                       queue (heavy-tailed scenario costs), per-warp engine
+ *                       state in shared memory; the engine itself is
+ *                       engine_core.h instantiated with the warp team below.
+ *   asb_ring_offsets  : device prefix sum of per-scenario FIFO/log sizes.
+ *
+ * Build: nvcc -gencode arch=compute_100a,code=sm_100a --fmad=false -O3
+ * (--fmad=false: the reference is Python, which never fuses multiply-add).
+ */
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/agentsim_b200.h"
+
+#define FULLMASK 0xffffffffu
+#define EC_DEV __device__ __forceinline__
+#define EC_LANE ((int)(threadIdx.x & 31))
+#define EC_TSIZE 32
+#define EC_NAN __longlong_as_double(0x7ff8000000000000ll)
+#define EC_INF __longlong_as_double(0x7ff0000000000000ll)
+#define EC_INF_BITS 0x7ff0000000000000ull
+
+EC_DEV void t_sync() { __syncwarp(); }
+EC_DEV unsigned t_ballot(bool p) { return __ballot_sync(FULLMASK, p); }
+EC_DEV unsigned t_lt_mask() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+EC_DEV int ec_popc(unsigned m) { return __popc(m); }
+EC_DEV long long t_bcast_ll(long long v, int src) { return __shfl_sync(FULLMASK, v, src); }
+EC_DEV long long t_scan_add_ll(long long v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long n = __shfl_up_sync(FULLMASK, v, o);
+    if (EC_LANE >= o) v += n;
+  }
+  return v;
+}
+EC_DEV long long t_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+  return v;
+}
+EC_DEV unsigned long long t_shfl_xor_ull(unsigned long long v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
+EC_DEV long long t_shfl_xor_ll(long long v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
+EC_DEV int t_shfl_xor_i(int v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
+EC_DEV void t_atomic_min_ull(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
+EC_DEV int t_atomic_add_i(int* p, int v) { return atomicAdd(p, v); }
+EC_DEV bool ec_isnan(double x) { return isnan(x); }
+EC_DEV double ec_floor(double x) { return floor(x); }
+EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__double_as_longlong(x); }
+EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
+
+#include "engine_core.h"
+
+namespace {
+
+struct Workspace {
+  double *tp, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
+  long long *next_seq, *start_rank;
+  int *next_prio, *sa, *logpos, *alive;
+  int *ring, *log;
+  long long* ring_off;
+  int* work;
+};
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+/* carve the workspace; returns bytes used (ptrs filled when base != nullptr) */
+size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t total_ring, Workspace* w) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> unsigned char* {
+    unsigned char* p = base ? base + off : nullptr;
+    off += align_up(bytes > 0 ? bytes : 1);
+    return p;
+  };
+  size_t na = (size_t)(total_agents > 0 ? total_agents : 1);
+  Workspace t;
+  t.tp = (double*)take(na * 8);
+  t.issue = (double*)take(na * 8);
+  t.anchor = (double*)take(na * 8);
+  t.rem = (double*)take(na * 8);
+  t.done = (double*)take(na * 8);
+  t.next_t = (double*)take(na * 8);
+  t.notbefore = (double*)take(na * 8);
+  t.pissue = (double*)take(na * 8);
+  t.next_seq = (long long*)take(na * 8);
+  t.start_rank = (long long*)take(na * 8);
+  t.next_prio = (int*)take(na * 4);
+  t.sa = (int*)take(na * 4);
+  t.logpos = (int*)take(na * 4);
+  t.alive = (int*)take(na * 4);
+  t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
+  t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
+  t.ring_off = (long long*)take((size_t)(n_scen + 1) * 8);
+  t.work = (int*)take(64);
+  if (w) *w = t;
+  return off;
+}
+
+__global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const int64_t* trace_agent_off,
+                                    long long* ring_off, int* work) {
+  /* single block: chunked exclusive scan of n_instances * n_agents */
+  __shared__ long long part[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (n_scen + nt - 1) / nt;
+  const int s0 = tid * per, s1 = min(n_scen, s0 + per);
+  long long sum = 0;
+  for (int s = s0; s < s1; s++) {
+    const AsbScenario& sc = scen[s];
+    sum += (long long)sc.n_instances * (trace_agent_off[sc.trace_id + 1] - trace_agent_off[sc.trace_id]);
+  }
+  part[tid] = sum;
+  __syncthreads();
+  if (tid == 0) {
+    long long run = 0;
+    for (int i = 0; i < nt; i++) {
+      long long v = part[i];
+      part[i] = run;
+      run += v;
+    }
+    ring_off[n_scen] = run;
+    *work = 0;
+  }
+  __syncthreads();
+  long long run = part[tid];
+  for (int s = s0; s < s1; s++) {
+    ring_off[s] = run;
+    const AsbScenario& sc = scen[s];
+    run += (long long)sc.n_instances * (trace_agent_off[sc.trace_id + 1] - trace_agent_off[sc.trace_id]);
+  }
+}
+
+template <int MAXM, int RCAP, int DCAP, int ACAP, int WPB>
+__global__ void __launch_bounds__(WPB * 32)
+    asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
+                      AsbOutputs out, Workspace ws) {
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5;
+  W* w = reinterpret_cast<W*>(smem_raw + (size_t)warp * ((sizeof(W) + 15) / 16 * 16));
+  for (;;) {
+    int s = 0;
+    if (EC_LANE == 0) s = atomicAdd(ws.work, 1);
+    s = __shfl_sync(FULLMASK, s, 0);
+    if (s >= n_scen) break;
+    /* scenario parameters and frequency table into shared memory */
+    {
+      const int* src = reinterpret_cast<const int*>(&scen[s]);
+      int* dst = reinterpret_cast<int*>(&w->sc);
+      for (int j = EC_LANE; j < (int)(sizeof(AsbScenario) / 4); j += 32) dst[j] = src[j];
+    }
+    __syncwarp();
+    const AsbScenario& sc = w->sc;
+    {
+      const long long t0 = tb.table_off[sc.table_id];
+      for (int l = EC_LANE; l < sc.n_levels; l += 32) {
+        w->pr[l] = tb.prefill_rate[t0 + l];
+        w->dr[l] = tb.decode_rate[t0 + l];
+        w->act[l] = tb.active_power[t0 + l];
+        w->idle[l] = tb.idle_power[t0 + l];
+      }
+    }
+    asb::GP g;
+    const long long a0 = tp.trace_agent_off[sc.trace_id];
+    const int A = (int)(tp.trace_agent_off[sc.trace_id + 1] - a0);
+    const long long oa = out.agent_off[s], oi = out.inst_off[s];
+    g.arrival = tp.arrival + a0;
+    g.aturn = reinterpret_cast<const long long*>(tp.agent_turn_off) + a0;
+    g.prefill = tp.prefill;
+    g.decode = tp.decode;
+    g.tool = tp.tool;
+    g.arr_order = tp.arrival_order + a0;
+    g.turn_base = tp.trace_turn_off[sc.trace_id];
+    g.ctime = out.completion_time + oa;
+    g.llm = out.llm_time + oa;
+    g.tp = ws.tp + oa;
+    g.issue = ws.issue + oa;
+    g.anchor = ws.anchor + oa;
+    g.rem = ws.rem + oa;
+    g.done = ws.done + oa;
+    g.next_t = ws.next_t + oa;
+    g.notbefore = ws.notbefore + oa;
+    g.pissue = ws.pissue + oa;
+    g.dec = reinterpret_cast<long long*>(out.decode_total) + oa;
+    g.maxctx = reinterpret_cast<long long*>(out.max_context) + oa;
+    g.ctx = reinterpret_cast<long long*>(out.context) + oa;
+    g.next_seq = ws.next_seq + oa;
+    g.start_rank = ws.start_rank + oa;
+    g.steps = out.turns_completed + oa;
+    g.inst = out.final_instance + oa;
+    g.mig = out.migrations + oa;
+    g.phase = out.phase + oa;
+    g.rank = out.arrival_rank + oa;
+    g.next_prio = ws.next_prio + oa;
+    g.sa = ws.sa + oa;
+    g.logpos = ws.logpos + oa;
+    g.alive = ws.alive + oa;
+    g.ring = ws.ring + ws.ring_off[s];
+    g.log = ws.log + ws.ring_off[s];
+    g.turn_issue = out.turn_issue ? out.turn_issue + out.turn_off[s] : nullptr;
+    g.turn_done = out.turn_done ? out.turn_done + out.turn_off[s] : nullptr;
+    g.dec_rows = out.decisions ? out.decisions + out.dec_off[s] : nullptr;
+    g.o_energy = out.energy + oi;
+    g.o_thr = out.thrash_time + oi;
+    g.o_usage = reinterpret_cast<long long*>(out.final_usage) + oi;
+    g.o_pending = out.final_pending + oi;
+    g.o_level = out.final_level + oi;
+    g.o_ctr = reinterpret_cast<long long*>(out.counters) + (long long)s * ASB_NCOUNTERS;
+    g.A = A;
+    g.M = sc.n_instances;
+    g.L = sc.n_levels;
+    __syncwarp();
+    asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
+    __syncwarp();
+  }
+}
+
+template <int MAXM, int RCAP, int DCAP, int ACAP, int WPB>
+int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp, const AsbTablePool& tb,
+                  const AsbOutputs& out, const Workspace& ws, cudaStream_t st) {
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP>;
+  static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
+  static_assert((RCAP & (RCAP - 1)) == 0, "RCAP must be a power of two");
+  const size_t per_warp = (sizeof(W) + 15) / 16 * 16;
+  const size_t smem = per_warp * WPB;
+  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, WPB>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return ASB_ERR_LAUNCH;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem) != cudaSuccess || per_sm < 1)
+    return ASB_ERR_LAUNCH;
+  long long want = (n_scen + WPB - 1) / WPB;
+  long long cap = (long long)sms * per_sm;
+  int blocks = (int)(want < cap ? want : cap);
+  if (blocks < 1) blocks = 1;
+  kern<<<blocks, WPB * 32, smem, st>>>(d_scen, n_scen, tp, tb, out, ws);
+  return cudaGetLastError() == cudaSuccess ? ASB_OK : ASB_ERR_LAUNCH;
+}
+
+}  // namespace
+
+extern "C" {
+
+int asb_abi_version(void) { return ASB_ABI_VERSION; }
+
+size_t asb_workspace_bytes(int32_t n_scen, int64_t total_agents, int64_t total_ring_slots) {
+  return carve(nullptr, n_scen, total_agents, total_ring_slots, nullptr);
+}
+
+int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_instances, AsbTracePool traces,
+                      AsbTablePool tables, AsbOutputs out, int64_t total_agents, int64_t total_ring_slots,
+                      void* d_workspace, size_t workspace_bytes, void* stream) {
+  if (n_scen < 0 || max_instances < 1 || max_instances > 64) return ASB_ERR_ARG;
+  if (n_scen == 0) return ASB_OK;
+  size_t need = carve(nullptr, n_scen, total_agents, total_ring_slots, nullptr);
+  if (!d_workspace || workspace_bytes < need) return ASB_ERR_WORKSPACE;
+  Workspace ws;
+  carve((unsigned char*)d_workspace, n_scen, total_agents, total_ring_slots, &ws);
+  cudaStream_t st = (cudaStream_t)stream;
+  ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
+  if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
+  if (max_instances <= 16)
+    return launch_engine<16, 256, 128, 64, 4>(d_scen, n_scen, traces, tables, out, ws, st);
+  return launch_engine<64, 256, 128, 64, 4>(d_scen, n_scen, traces, tables, out, ws, st);
+}
+
+}  // extern "C"

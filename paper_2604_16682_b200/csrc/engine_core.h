@@ -1,0 +1,1317 @@
+/*
+ * engine_core.h — the batched, epoch-synchronous scenario engine.
+ *
+ * One TEAM (a warp on the GPU) runs one scenario = one reference
+ * `run_simulation` (/root/reference/pkg/src/agentsim/engine.py:576-604).
+ * The reference pops one event at a time from a global heap; this engine
+ * reproduces exactly the same event order and arithmetic, but processes the
+ * events between two control epochs as an optimistic batch:
+ *
+ *   1. epoch event (engine.py:436-488): the agent-tick sweep computes every
+ *      instance's min running throughput over its ongoing ∪ pending agents
+ *      (controller.py:96-103) in one pass over the alive list; level select,
+ *      SLO boost, β/γ admission (a prefix scan over the pending FIFO) and the
+ *      admitted turn starts run with lane-parallel helpers;
+ *   2. due collection: agents whose next event falls before the next epoch;
+ *   3. speculation (lane per agent): each agent's own event chain
+ *      (complete → tool gap → next turn → …, engine.py:374-401, 509-568)
+ *      inside the window, assuming the instance's thrash flag and level stay
+ *      as they are — the only instance state an agent's timing reads;
+ *   4. sort the records by (time, priority); ties are ordered by the
+ *      reference's push sequence number (engine.py:300-301) during
+ *      5. the commit walk (one lane): usage / running-count / power / router
+ *      bookkeeping in exact reference order, stopping before the first event
+ *      that couples agents (a completion that flips the thrash flag, a
+ *      reassignment check that migrates, or any start/complete under
+ *      interference) — that event is executed serially with the exact
+ *      handler semantics, and speculation restarts after it;
+ *   6. apply (lane per agent): committed chain prefixes are written back.
+ *
+ * The file is compiled twice: by nvcc for sm_100a with the warp team
+ * (engine.cu), and by g++ with a 1-lane team (tests/native/host_engine.cpp)
+ * purely as a test harness for the batching logic on CPU.  The host build is
+ * never loaded by the package.
+ *
+ * Arithmetic follows the reference operation by operation in IEEE binary64
+ * (no FMA contraction: built with --fmad=false / -ffp-contract=off).
+ */
+#ifndef ASB_ENGINE_CORE_H
+#define ASB_ENGINE_CORE_H
+
+#include "../../include/agentsim_b200.h"
+
+/* ---- team primitives: provided by the includer ----------------------------
+ *   EC_DEV, EC_LANE, EC_TSIZE, t_sync(), t_ballot(p), t_lt_mask(),
+ *   t_bcast_i(v,src), t_bcast_ll(v,src), t_scan_add_ll(v), t_sum_ll(v),
+ *   t_min_ull(v), t_atomic_min_ull(p,v), t_atomic_add_i(p,v), ec_isnan(x),
+ *   ec_floor(x), EC_NAN, EC_INF
+ */
+
+namespace asb {
+
+enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4 };
+enum { F_LAST = 1, F_CHECK = 2, F_COMMITTED = 4 };
+enum { STOP_NONE = 0, STOP_COUPLING = 1, STOP_HORIZON = 2, STOP_LOGFULL = 3 };
+
+/* one speculative event record (engine.py handler invocation) */
+struct Rec {
+  double t;
+  long long seq;       /* own push sequence number (-1 until known) */
+  long long push_seq;  /* seq of the event this one pushes */
+  long long aux64;     /* COMPLETE: context after growth; start: start rank */
+  int agent;
+  short prio;          /* EV_* kind == tie-break priority */
+  short flags;
+  int delta;           /* COMPLETE: prefill+decode */
+  int child;           /* next record of the same agent chain, -1 none */
+  int logpos;          /* start: position in the instance running log */
+  int inst;
+};
+
+struct SortE {
+  unsigned long long tb; /* time bits (times are >= 0, so bits order like values) */
+  unsigned int prio;
+  unsigned int idx;
+};
+
+/* per-instance engine state: InstanceState (instance.py:163-181) + _Instance (engine.py:234-247) */
+struct Inst {
+  long long usage;
+  double watts, t_pow, energy, thr_since, thr_time;
+  int level, running, thr, thr_flag;
+  int key_valid, key_level, key_thr, key_run;
+  int fifo_head, fifo_len, log_len, pad_;
+};
+
+/* pointers for one scenario (row bases applied) */
+struct GP {
+  /* trace */
+  const double* arrival;
+  const long long* aturn;  /* [A+1] global turn offsets */
+  const int* prefill;
+  const int* decode;
+  const double* tool;
+  const int* arr_order;
+  long long turn_base;
+  /* agent state (SoA) */
+  double *ctime, *llm, *tp, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
+  long long *dec, *maxctx, *ctx, *next_seq, *start_rank;
+  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos;
+  int* alive;
+  int* ring;  /* [M*A] pending FIFOs */
+  int* log;   /* [M*A] running logs (insertion order of inst.running) */
+  /* outputs */
+  double *turn_issue, *turn_done;
+  AsbDecision* dec_rows;
+  double *o_energy, *o_thr;
+  long long* o_usage;
+  int *o_pending, *o_level;
+  long long* o_ctr;
+  int A, M, L;
+};
+
+template <int MAXM, int RCAP, int DCAP, int ACAP>
+struct WS {
+  AsbScenario sc;
+  double now, bound;
+  long long seq, start_ctr;
+  long long ctr[ASB_NCOUNTERS];
+  unsigned long long hz_t;
+  int hz_p;
+  long long hz_s;
+  int n_alive, rr_next, arr_ptr, arr_rank, status, incl;
+  int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i;
+  long long tmp_ll;
+  double pr[16], dr[16], act[16], idle[16];
+  Inst in[MAXM];
+  unsigned long long tmin[MAXM];
+  int due[DCAP];
+  Rec rec[RCAP];
+  SortE srt[RCAP];
+  Rec stop_r;
+};
+
+/* ----------------------------------------------------------------------------
+ * small scalar helpers (any lane)
+ * -------------------------------------------------------------------------- */
+
+template <class W>
+EC_DEV double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
+  /* service_time, instance.py:184-204 */
+  double base = (double)g.prefill[turn] / w->pr[level - 1] + (double)g.decode[turn] / w->dr[level - 1];
+  int extra = concurrent - 1 > 0 ? concurrent - 1 : 0;
+  double factor = 1.0 + w->sc.interference * (double)extra;
+  if (thr) factor *= w->sc.thrash_factor;
+  return base * factor;
+}
+
+template <class W>
+EC_DEV void update_power(W* w, int i, double now) {
+  /* _update_power, engine.py:321-327 (lane 0) */
+  Inst& in = w->in[i - 1];
+  double wt = in.running > 0 ? w->act[in.level - 1] : w->idle[in.level - 1];
+  if (wt != in.watts) {
+    in.energy += in.watts * (now - in.t_pow);
+    in.t_pow = now;
+    in.watts = wt;
+  }
+}
+
+template <class W>
+EC_DEV void sync_thrash(W* w, int i, double now) {
+  /* _sync_thrash, engine.py:329-336 (lane 0) */
+  Inst& in = w->in[i - 1];
+  if (in.thr != in.thr_flag) {
+    if (in.thr_flag)
+      in.thr_time += now - in.thr_since;
+    else
+      in.thr_since = now;
+    in.thr_flag = in.thr;
+    w->ctr[ASB_CTR_THRASH_FLIPS]++;
+  }
+}
+
+/* lexicographic argmin over (usage, id), router.py:91,123,150; cand_mode:
+ * 0 all instances, 1 reassignment candidates (usage > 0 or current) */
+template <class W>
+EC_DEV int argmin_usage(const W* w, int cand_mode, int current) {
+  int best = 0;
+  long long bu = 0;
+  for (int i = 1; i <= w->sc.n_instances; i++) {
+    long long u = w->in[i - 1].usage;
+    if (cand_mode == 1 && !(u > 0 || i == current)) continue;
+    if (!best || u < bu) {
+      best = i;
+      bu = u;
+    }
+  }
+  return best;
+}
+
+/* maybe_reassign decision given the counter already reached the interval
+ * (router.py:110-128): returns the target or 0 */
+template <class W>
+EC_DEV int reassign_target(const W* w, int current) {
+  int best = argmin_usage(w, w->sc.include_idle ? 0 : 1, current);
+  if (best && best != current &&
+      (double)w->in[current - 1].usage >= w->sc.imbalance_ratio * (double)w->in[best - 1].usage)
+    return best;
+  return 0;
+}
+
+/* arrival routing, engine.py:496-503 / router.py:75-94,131-151 (lane 0) */
+template <class W>
+EC_DEV int route_arrival(W* w) {
+  const AsbScenario& sc = w->sc;
+  if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
+    int t = (w->rr_next % sc.n_instances) + 1;
+    w->rr_next++;
+    return t;
+  }
+  if (sc.policy == ASB_POLICY_LEAST_LOADED) return argmin_usage(w, 0, 0);
+  double threshold = sc.consolidation_threshold * (double)sc.capacity;
+  for (int i = 1; i <= sc.n_instances; i++)
+    if ((double)w->in[i - 1].usage < threshold) return i;
+  return argmin_usage(w, 0, 0);
+}
+
+/* ----------------------------------------------------------------------------
+ * running log: insertion-ordered `inst.running` (engine.py:239, 398, 517)
+ * -------------------------------------------------------------------------- */
+
+/* Iterate instance i's running log in insertion order; live entries are
+ * compacted to the front; if `retime`, each live turn is re-timed
+ * (engine.py:355-372) with consecutive push sequence numbers. (team) */
+template <class W>
+EC_DEV void log_pass(W* w, const GP& g, int i, int retime) {
+  Inst& in = w->in[i - 1];
+  const int len = in.log_len;
+  int* lg = g.log + (long long)(i - 1) * g.A;
+  const double now = w->now;
+  const long long seq0 = w->seq;
+  const int level = in.level, running = in.running, thr = in.thr;
+  int out = 0;
+  for (int base = 0; base < len; base += EC_TSIZE) {
+    int p = base + EC_LANE;
+    int a = -1;
+    bool live = false;
+    if (p < len) {
+      a = lg[p];
+      live = g.phase[a] == ASB_PHASE_RUNNING && g.inst[a] == i && g.logpos[a] == p;
+    }
+    unsigned m = t_ballot(live);
+    int pos = out + ec_popc(m & t_lt_mask());
+    t_sync(); /* every lane has read its entry before any entry is rewritten */
+    if (live) {
+      if (retime) {
+        double anchor = g.anchor[a], done = g.done[a], rem = g.rem[a];
+        double segment = done - anchor;
+        if (segment > 0) {
+          double fraction_done = (now - anchor) / segment;
+          double x = 1.0 - fraction_done;
+          rem *= (x > 0.0 ? x : 0.0);
+        }
+        long long turn = g.aturn[a] + g.steps[a];
+        double full = svc_time(w, g, turn, level, running, thr);
+        done = now + rem * full;
+        g.anchor[a] = now;
+        g.rem[a] = rem;
+        g.done[a] = done;
+        g.next_t[a] = done;
+        g.next_prio[a] = EV_COMPLETE;
+        g.next_seq[a] = seq0 + pos;
+      }
+      g.logpos[a] = pos;
+      lg[pos] = a;
+    }
+    out += ec_popc(m);
+    t_sync();
+  }
+  if (EC_LANE == 0) {
+    in.log_len = out;
+    if (retime) {
+      w->seq += out;
+      w->ctr[ASB_CTR_RETIMES] += out;
+    }
+  }
+  t_sync();
+}
+
+/* _conditions_changed, engine.py:344-372 (team) */
+template <class W>
+EC_DEV void cond_changed(W* w, const GP& g, int i) {
+  if (EC_LANE == 0) {
+    Inst& in = w->in[i - 1];
+    int kr = w->sc.interference > 0 ? in.running : 0;
+    int changed = !(in.key_valid && in.key_level == in.level && in.key_thr == in.thr && in.key_run == kr);
+    if (changed) {
+      in.key_valid = 1;
+      in.key_level = in.level;
+      in.key_thr = in.thr;
+      in.key_run = kr;
+    }
+    w->flag = changed && in.log_len > 0;
+  }
+  t_sync();
+  if (w->flag) log_pass(w, g, i, 1);
+}
+
+/* append agent a to instance i's running log (lane 0); returns position */
+template <class W>
+EC_DEV int log_append(W* w, const GP& g, int i, int a) {
+  Inst& in = w->in[i - 1];
+  int p = in.log_len++;
+  g.log[(long long)(i - 1) * g.A + p] = a;
+  return p;
+}
+
+/* ----------------------------------------------------------------------------
+ * serial handlers (exact reference semantics on committed state) — team
+ * -------------------------------------------------------------------------- */
+
+/* _start_turn, engine.py:374-401 */
+template <class W>
+EC_DEV void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
+  if (EC_LANE == 0) w->in[i - 1].running += 1;
+  t_sync();
+  cond_changed(w, g, i);
+  if (w->in[i - 1].log_len >= g.A) log_pass(w, g, i, 0);
+  if (EC_LANE == 0) {
+    Inst& in = w->in[i - 1];
+    double now = w->now;
+    long long turn = g.aturn[a] + g.steps[a];
+    double dur = svc_time(w, g, turn, in.level, in.running, in.thr);
+    g.issue[a] = issue;
+    g.anchor[a] = now;
+    g.rem[a] = 1.0;
+    g.done[a] = now + dur;
+    g.phase[a] = ASB_PHASE_RUNNING;
+    g.next_t[a] = now + dur;
+    g.next_prio[a] = EV_COMPLETE;
+    g.next_seq[a] = w->seq++;
+    g.start_rank[a] = w->start_ctr++;
+    g.logpos[a] = log_append(w, g, i, a);
+    update_power(w, i, now);
+  }
+  t_sync();
+}
+
+/* _on_complete, engine.py:509-535 */
+template <class W>
+EC_DEV void complete_serial(W* w, const GP& g, int a) {
+  int i = g.inst[a];
+  if (EC_LANE == 0) {
+    Inst& in = w->in[i - 1];
+    double now = w->now;
+    in.running -= 1;
+    double llm = now - g.issue[a];
+    long long turn = g.aturn[a] + g.steps[a];
+    int p = g.prefill[turn], d = g.decode[turn];
+    long long ctx = g.ctx[a] + p + d;
+    int steps = g.steps[a] + 1;
+    long long dec = g.dec[a] + d;
+    double lt = g.llm[a] + llm;
+    g.ctx[a] = ctx;
+    g.steps[a] = steps;
+    g.dec[a] = dec;
+    g.llm[a] = lt;
+    if (ctx > g.maxctx[a]) g.maxctx[a] = ctx;
+    in.usage += p + d;
+    w->ctr[ASB_CTR_TURNS]++;
+    w->ctr[ASB_CTR_EVENTS]++;
+    if (g.turn_issue) {
+      long long lt_idx = turn - g.turn_base;
+      g.turn_issue[lt_idx] = g.issue[a];
+      g.turn_done[lt_idx] = now;
+    }
+    int n_turns = (int)(g.aturn[a + 1] - g.aturn[a]);
+    if (steps == n_turns) {
+      in.usage -= ctx;
+      g.phase[a] = ASB_PHASE_DONE;
+      g.ctime[a] = now;
+      g.tp[a] = EC_NAN;
+      g.next_prio[a] = 0;
+      w->ctr[ASB_CTR_COMPLETED]++;
+    } else {
+      g.phase[a] = ASB_PHASE_TOOL;
+      g.tp[a] = (double)dec / lt;
+      g.next_t[a] = now + g.tool[turn];
+      g.next_prio[a] = EV_TOOL;
+      g.next_seq[a] = w->seq++;
+    }
+    in.thr = in.usage > w->sc.capacity;
+    sync_thrash(w, i, now);
+  }
+  t_sync();
+  cond_changed(w, g, i);
+  if (EC_LANE == 0) update_power(w, i, w->now);
+  t_sync();
+}
+
+/* _on_tool, engine.py:537-561 */
+template <class W>
+EC_DEV void tool_serial(W* w, const GP& g, int a) {
+  int source = g.inst[a];
+  if (EC_LANE == 0) {
+    int target = 0;
+    w->ctr[ASB_CTR_EVENTS]++;
+    if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
+      int sa = g.sa[a] + 1;
+      if (sa >= w->sc.reassign_interval) {
+        target = reassign_target(w, source);
+        if (target || !w->sc.reset_only_on_reassign) sa = 0;
+      }
+      g.sa[a] = sa;
+    }
+    w->tmp_i = target;
+    if (target) {
+      double now = w->now;
+      Inst& src = w->in[source - 1];
+      Inst& dst = w->in[target - 1];
+      g.mig[a] += 1;
+      w->ctr[ASB_CTR_MIGRATIONS]++;
+      /* migrate_context, router.py:154-176 */
+      src.usage -= g.ctx[a];
+      src.thr = src.usage > w->sc.capacity;
+      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
+      dst.fifo_len++;
+      g.inst[a] = target;
+      g.phase[a] = ASB_PHASE_PENDING;
+      g.pissue[a] = now;
+      g.notbefore[a] = now + w->sc.migration_delay;
+      g.next_prio[a] = 0;
+      sync_thrash(w, source, now);
+    }
+  }
+  t_sync();
+  if (!w->tmp_i) {
+    start_turn_serial(w, g, source, a, w->now);
+    return;
+  }
+  cond_changed(w, g, source);
+  if (EC_LANE == 0) update_power(w, source, w->now);
+  t_sync();
+}
+
+template <class W>
+EC_DEV void exec_serial(W* w, const GP& g, const Rec& r) {
+  if (EC_LANE == 0) w->now = r.t;
+  t_sync();
+  if (r.prio == EV_COMPLETE) {
+    complete_serial(w, g, r.agent);
+  } else if (r.prio == EV_TOOL) {
+    tool_serial(w, g, r.agent);
+  } else {
+    if (EC_LANE == 0) w->ctr[ASB_CTR_EVENTS]++;
+    t_sync();
+    start_turn_serial(w, g, g.inst[r.agent], r.agent, g.issue[r.agent]);
+  }
+}
+
+/* ----------------------------------------------------------------------------
+ * speculation cursor: one agent's own event chain (lane-local)
+ * -------------------------------------------------------------------------- */
+
+struct Cur {
+  int a, inst, phase, prio, steps, n_turns, sa;
+  double t, llm, issue, anchor, rem, done;
+  long long ctx, dec, maxctx, turn0;
+};
+
+EC_DEV void cur_load(const GP& g, Cur& c, int a) {
+  c.a = a;
+  c.inst = g.inst[a];
+  c.phase = g.phase[a];
+  c.prio = g.next_prio[a];
+  c.t = g.next_t[a];
+  c.steps = g.steps[a];
+  c.turn0 = g.aturn[a];
+  c.n_turns = (int)(g.aturn[a + 1] - c.turn0);
+  c.sa = g.sa[a];
+  c.llm = g.llm[a];
+  c.issue = g.issue[a];
+  c.anchor = g.anchor[a];
+  c.rem = g.rem[a];
+  c.done = g.done[a];
+  c.ctx = g.ctx[a];
+  c.dec = g.dec[a];
+  c.maxctx = g.maxctx[a];
+}
+
+/* Advance the cursor over its next event, filling record r.  Mirrors the
+ * agent-local part of _on_complete / _on_tool / _on_delayed_start. Returns
+ * false on an event-order violation (child scheduled at or before parent). */
+template <class W>
+EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
+  r.t = c.t;
+  r.prio = (short)c.prio;
+  r.agent = c.a;
+  r.inst = c.inst;
+  r.flags = 0;
+  r.child = -1;
+  if (c.prio == EV_COMPLETE) {
+    long long turn = c.turn0 + c.steps;
+    int p = g.prefill[turn], d = g.decode[turn];
+    double llm = c.t - c.issue;
+    if (apply && g.turn_issue) {
+      g.turn_issue[turn - g.turn_base] = c.issue;
+      g.turn_done[turn - g.turn_base] = c.t;
+    }
+    c.ctx += p + d;
+    c.steps += 1;
+    c.dec += d;
+    c.llm += llm;
+    if (c.ctx > c.maxctx) c.maxctx = c.ctx;
+    r.delta = p + d;
+    r.aux64 = c.ctx;
+    if (c.steps == c.n_turns) {
+      r.flags |= F_LAST;
+      c.phase = ASB_PHASE_DONE;
+      c.prio = 0;
+    } else {
+      c.phase = ASB_PHASE_TOOL;
+      c.prio = EV_TOOL;
+      c.t = c.t + g.tool[turn];
+    }
+    return true;
+  }
+  /* EV_TOOL (issue = now) or EV_ISSUE (issue carried in c.issue) */
+  if (c.prio == EV_TOOL) {
+    c.issue = c.t;
+    if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
+      c.sa += 1;
+      if (c.sa >= w->sc.reassign_interval) {
+        r.flags |= F_CHECK;
+        if (!w->sc.reset_only_on_reassign) c.sa = 0;
+      }
+    }
+  }
+  const Inst& in = w->in[c.inst - 1];
+  double dur = svc_time(w, g, c.turn0 + c.steps, in.level, in.running, in.thr);
+  double t0 = c.t;
+  c.anchor = t0;
+  c.rem = 1.0;
+  c.done = t0 + dur;
+  c.phase = ASB_PHASE_RUNNING;
+  c.prio = EV_COMPLETE;
+  c.t = c.done;
+  return c.t > t0;
+}
+
+/* ----------------------------------------------------------------------------
+ * one scenario
+ * -------------------------------------------------------------------------- */
+
+EC_DEV bool key_less(unsigned long long ta, unsigned pa, unsigned long long tb, unsigned pb) {
+  return ta < tb || (ta == tb && pa < pb);
+}
+
+template <class W>
+EC_DEV bool is_due(const W* w, double t) {
+  return w->incl ? (t <= w->bound) : (t < w->bound);
+}
+
+/* agent-tick sweep: per-instance count and min running throughput over the
+ * alive list (ongoing ∪ pending of every instance), with lazy compaction of
+ * finished agents.  controller.py:89-103, engine.py:437-454 (team) */
+template <class W>
+EC_DEV void tick_sweep(W* w, const GP& g) {
+  const int M = w->sc.n_instances;
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS;
+  t_sync();
+  const int n = w->n_alive;
+  int cur_i = 0, dead = 0;
+  unsigned long long cur_m = EC_INF_BITS;
+  for (int j = EC_LANE; j < n; j += EC_TSIZE) {
+    int a = g.alive[j];
+    double tp = g.tp[a];
+    if (ec_isnan(tp)) {
+      dead++;
+      continue;
+    }
+    int i = g.inst[a];
+    if (i != cur_i) {
+      if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
+      cur_i = i;
+      cur_m = EC_INF_BITS;
+    }
+    unsigned long long b = ec_bits(tp);
+    if (b < cur_m) cur_m = b;
+  }
+  if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
+  long long dead_all = t_sum_ll(dead);
+  t_sync();
+  if (EC_LANE == 0) w->ctr[ASB_CTR_TICKS] += n - dead_all;
+  if (dead_all * 4 > n && dead_all > 0) {
+    /* order-free compaction of the alive list (in place: write index <= read index) */
+    int out = 0;
+    for (int base = 0; base < n; base += EC_TSIZE) {
+      int j = base + EC_LANE;
+      int a = j < n ? g.alive[j] : -1;
+      bool live = a >= 0 && !ec_isnan(g.tp[a]);
+      unsigned m = t_ballot(live);
+      t_sync();
+      if (live) g.alive[out + ec_popc(m & t_lt_mask())] = a;
+      out += ec_popc(m);
+      t_sync();
+    }
+    if (EC_LANE == 0) w->n_alive = out;
+  }
+  t_sync();
+}
+
+/* β/γ FIFO admission as a prefix scan (controller.py:112-130); returns count (team) */
+template <class W>
+EC_DEV int admission(W* w, const GP& g, int i, double gcap) {
+  Inst& in = w->in[i - 1];
+  const int len = in.fifo_len, head = in.fifo_head;
+  const int* ring = g.ring + (long long)(i - 1) * g.A;
+  long long usage = in.usage;
+  int n_adm = 0;
+  for (int base = 0; base < len; base += EC_TSIZE) {
+    int j = base + EC_LANE;
+    bool valid = j < len;
+    int a = valid ? ring[(head + j) % g.A] : -1;
+    long long c = valid ? g.ctx[a] : 0;
+    long long incl = t_scan_add_ll(c);
+    long long excl = incl - c;
+    bool ok = valid && (double)(usage + excl) < gcap;
+    unsigned m = t_ballot(ok);
+    int cnt = ec_popc(m);
+    if (cnt) usage += t_bcast_ll(incl, cnt - 1);
+    n_adm += cnt;
+    if (cnt < EC_TSIZE) break;
+  }
+  t_sync();
+  if (EC_LANE == 0) {
+    in.usage = usage;
+    in.fifo_head = (head + n_adm) % (g.A > 0 ? g.A : 1);
+    in.fifo_len = len - n_adm;
+    in.thr = usage > w->sc.capacity;
+  }
+  t_sync();
+  return n_adm;
+}
+
+/* _on_epoch, engine.py:436-488 + control_epoch, controller.py:133-186 (team) */
+template <class W>
+EC_DEV void epoch_event(W* w, const GP& g, long long k) {
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances, L = sc.n_levels;
+  tick_sweep(w, g);
+  for (int i = 1; i <= M; i++) {
+    Inst& in = w->in[i - 1];
+    const long long usage_obs = in.usage;
+    const bool has_tp = w->tmin[i - 1] != EC_INF_BITS;
+    const double min_tp = has_tp ? ec_from_bits(w->tmin[i - 1]) : EC_NAN;
+    int level;
+    if (sc.variant == ASB_VARIANT_OFF)
+      level = L;
+    else if (sc.variant == ASB_VARIANT_FIXED)
+      level = sc.fixed_level;
+    else {
+      /* select_frequency_level, controller.py:81-86 */
+      double ac = sc.alpha * (double)sc.capacity;
+      if ((double)usage_obs >= ac)
+        level = L;
+      else
+        level = (int)ec_floor((double)usage_obs / ac * (double)(L - 1)) + 1;
+    }
+    int boosted = 0;
+    if (sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.boost_enabled && has_tp && min_tp < sc.slo_target) {
+      level = L;
+      boosted = 1;
+    }
+    t_sync();
+    if (EC_LANE == 0) in.level = level;
+    t_sync();
+    cond_changed(w, g, i);
+    if (EC_LANE == 0) update_power(w, i, w->now);
+    t_sync();
+    double gamma = 1.0, beta = 1.0;
+    if (sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.thrash_avoidance) {
+      gamma = sc.gamma;
+      beta = sc.beta;
+    }
+    const int head0 = in.fifo_head;
+    const int n_adm = admission(w, g, i, gamma * (double)sc.capacity);
+    const int deferred = (double)in.usage > beta * (double)sc.capacity;
+    if (EC_LANE == 0) sync_thrash(w, i, w->now);
+    t_sync();
+    cond_changed(w, g, i);
+    /* start the admitted agents' turns in admission order (engine.py:458-473) */
+    if (sc.interference > 0) {
+      for (int j = 0; j < n_adm; j++) {
+        int a = g.ring[(long long)(i - 1) * g.A + (head0 + j) % g.A];
+        double issue = ec_isnan(g.pissue[a]) ? w->now : g.pissue[a];
+        t_sync();
+        if (EC_LANE == 0) g.pissue[a] = EC_NAN;
+        if (w->now < g.notbefore[a]) {
+          if (EC_LANE == 0) {
+            g.phase[a] = ASB_PHASE_WAITING_START;
+            g.issue[a] = issue;
+            g.next_t[a] = g.notbefore[a];
+            g.next_prio[a] = EV_ISSUE;
+            g.next_seq[a] = w->seq++;
+          }
+          t_sync();
+        } else {
+          start_turn_serial(w, g, i, a, issue);
+        }
+      }
+    } else if (n_adm > 0) {
+      if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0);
+      const long long seq0 = w->seq, rank0 = w->start_ctr;
+      const int log0 = in.log_len, lvl = in.level, thr = in.thr;
+      const double now = w->now;
+      int started = 0;
+      for (int base = 0; base < n_adm; base += EC_TSIZE) {
+        int j = base + EC_LANE;
+        bool valid = j < n_adm;
+        int a = valid ? g.ring[(long long)(i - 1) * g.A + (head0 + j) % g.A] : -1;
+        bool start = false;
+        double issue = 0.0;
+        if (valid) {
+          double pi = g.pissue[a];
+          issue = ec_isnan(pi) ? now : pi;
+          g.pissue[a] = EC_NAN;
+          start = !(now < g.notbefore[a]);
+        }
+        unsigned m = t_ballot(start);
+        int sidx = started + ec_popc(m & t_lt_mask());
+        if (valid) {
+          g.issue[a] = issue;
+          g.next_seq[a] = seq0 + j;
+          if (!start) {
+            g.phase[a] = ASB_PHASE_WAITING_START;
+            g.next_t[a] = g.notbefore[a];
+            g.next_prio[a] = EV_ISSUE;
+          } else {
+            double dur = svc_time(w, g, g.aturn[a] + g.steps[a], lvl, 0, thr);
+            g.anchor[a] = now;
+            g.rem[a] = 1.0;
+            g.done[a] = now + dur;
+            g.next_t[a] = now + dur;
+            g.next_prio[a] = EV_COMPLETE;
+            g.phase[a] = ASB_PHASE_RUNNING;
+            g.start_rank[a] = rank0 + sidx;
+            g.logpos[a] = log0 + sidx;
+            g.log[(long long)(i - 1) * g.A + log0 + sidx] = a;
+          }
+        }
+        started += ec_popc(m);
+      }
+      t_sync();
+      if (EC_LANE == 0) {
+        w->seq += n_adm;
+        w->start_ctr += started;
+        in.running += started;
+        in.log_len += started;
+      }
+      t_sync();
+    }
+    if (EC_LANE == 0) {
+      update_power(w, i, w->now);
+      if (g.dec_rows) {
+        AsbDecision& d = g.dec_rows[k * M + (i - 1)];
+        d.time = w->now;
+        d.min_throughput = min_tp;
+        d.usage_observed = usage_obs;
+        d.instance_id = i;
+        d.frequency_level = level;
+        d.admitted_count = n_adm;
+        d.pending_depth = in.fifo_len;
+        d.boosted = boosted;
+        d.deferred = deferred;
+      }
+    }
+    t_sync();
+  }
+}
+
+/* count alive agents whose next event is due before `bound` (team) */
+template <class W>
+EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
+  int c = 0;
+  for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
+    int a = g.alive[j];
+    if (g.next_prio[a] > 0) {
+      double t = g.next_t[a];
+      if (incl ? t <= bound : t < bound) c++;
+    }
+  }
+  return (int)t_sum_ll(c);
+}
+
+/* horizon key: records are committed only while (t, prio, seq) < (hz_t, hz_p, hz_s) */
+EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, unsigned long long ht,
+                          unsigned hp, long long hs) {
+  if (tb != ht) return tb < ht;
+  if (pr != hp) return pr < hp;
+  return seq < hs;
+}
+
+enum { BATCH_DONE = 0, BATCH_MORE = 1, BATCH_SERIAL = 2 };
+
+/* one optimistic batch inside the current window (team) */
+template <class W, int RCAP, int DCAP, int ACAP>
+EC_DEV int batch(W* w, const GP& g, double win_end) {
+  /* ---- 1. due collection (shrink the window if too many agents are due) */
+  double bound = win_end;
+  int incl = w->incl;
+  int nd = count_due(w, g, bound, incl);
+  if (nd > DCAP) {
+    /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
+    double lo = w->now, hi = bound;
+    int clo = 0;
+    for (int it = 0; it < 128; it++) {
+      double mid = lo + (hi - lo) * 0.5;
+      if (!(mid > lo && mid < hi)) break;
+      int c = count_due(w, g, mid, 0);
+      if (c > DCAP) {
+        hi = mid;
+      } else {
+        lo = mid;
+        clo = c;
+        if (c * 2 >= DCAP) break;
+      }
+    }
+    if (clo == 0) return BATCH_SERIAL; /* a same-timestamp burst larger than DCAP */
+    bound = lo;
+    incl = 0;
+  }
+  if (EC_LANE == 0) {
+    w->n_due = 0;
+    w->hz_t = EC_INF_BITS;
+    w->hz_p = 0;
+    w->hz_s = 0;
+  }
+  t_sync();
+  for (int base = 0; base < w->n_alive; base += EC_TSIZE) {
+    int j = base + EC_LANE;
+    bool due = false;
+    int a = -1;
+    if (j < w->n_alive) {
+      a = g.alive[j];
+      if (g.next_prio[a] > 0) {
+        double t = g.next_t[a];
+        due = incl ? t <= bound : t < bound;
+      }
+    }
+    unsigned m = t_ballot(due);
+    if (due) w->due[w->n_due + ec_popc(m & t_lt_mask())] = a;
+    t_sync();
+    if (EC_LANE == 0) w->n_due += ec_popc(m);
+    t_sync();
+  }
+  /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
+  if (EC_LANE == 0) {
+    int n_arr = 0;
+    int p = w->arr_ptr;
+    const double T = w->sc.sim_duration;
+    while (p < g.A) {
+      int a = g.arr_order[p];
+      double t = g.arrival[a];
+      if (!(t < T)) break;
+      if (!(incl ? t <= bound : t < bound)) break;
+      if (n_arr == ACAP) {
+        unsigned long long tb = ec_bits(t);
+        if (below_horizon(tb, EV_ARRIVAL, p, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+          w->hz_t = tb;
+          w->hz_p = EV_ARRIVAL;
+          w->hz_s = p;
+        }
+        break;
+      }
+      Rec& r = w->rec[w->n_due + n_arr];
+      r.t = t;
+      r.prio = EV_ARRIVAL;
+      r.agent = a;
+      r.seq = p; /* arrivals tie-break by trace order (engine.py:315-317) */
+      r.flags = 0;
+      r.child = -1;
+      r.inst = 0;
+      n_arr++;
+      p++;
+    }
+    w->n_arr = n_arr;
+    w->n_rec = w->n_due + n_arr;
+    w->tmp_i = 0;
+  }
+  t_sync();
+  /* ---- 3. speculation: each lane runs its due agents' chains */
+  unsigned long long my_hz_t = EC_INF_BITS;
+  unsigned my_hz_p = 0;
+  int order_err = 0;
+  const int nd2 = w->n_due;
+  const int nr0 = w->n_rec;
+  for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
+    Cur c;
+    cur_load(g, c, w->due[d]);
+    Rec* r = &w->rec[d];
+    r->seq = g.next_seq[c.a];
+    if (!cur_step(w, g, c, *r, false)) order_err = 1;
+    while (c.prio > 0 && (incl ? c.t <= bound : c.t < bound)) {
+      int slot = t_atomic_add_i(&w->tmp_i, 1) + nr0;
+      if (slot >= RCAP) {
+        /* dropped continuation: its seq is unknown, so nothing at its
+         * (time, prio) may commit in this batch */
+        unsigned long long tb = ec_bits(c.t);
+        if (key_less(tb, (unsigned)c.prio, my_hz_t, my_hz_p)) {
+          my_hz_t = tb;
+          my_hz_p = (unsigned)c.prio;
+        }
+        break;
+      }
+      r->child = slot;
+      r = &w->rec[slot];
+      r->seq = -1;
+      if (!cur_step(w, g, c, *r, false)) order_err = 1;
+    }
+  }
+  {
+    unsigned long long k = my_hz_t;
+    unsigned kp = my_hz_p;
+    for (int off = EC_TSIZE / 2; off > 0; off >>= 1) {
+      unsigned long long ok = t_shfl_xor_ull(k, off);
+      unsigned okp = (unsigned)t_shfl_xor_i((int)kp, off);
+      if (key_less(ok, okp, k, kp)) {
+        k = ok;
+        kp = okp;
+      }
+    }
+    int oe = (int)t_sum_ll(order_err);
+    t_sync();
+    if (EC_LANE == 0) {
+      if (below_horizon(k, kp, -1, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+        w->hz_t = k;
+        w->hz_p = (int)kp;
+        w->hz_s = -1;
+      }
+      int extra = w->tmp_i;
+      w->n_rec = nr0 + (extra < RCAP - nr0 ? extra : RCAP - nr0);
+      if (oe) w->status = ASB_SIMERR_ORDER;
+    }
+    t_sync();
+  }
+  /* ---- 4. sort by (time, prio) — bitonic over the next power of two */
+  const int n = w->n_rec;
+  int np2 = 1;
+  while (np2 < n) np2 <<= 1;
+  for (int j = EC_LANE; j < np2; j += EC_TSIZE) {
+    SortE& e = w->srt[j];
+    if (j < n) {
+      e.tb = ec_bits(w->rec[j].t);
+      e.prio = (unsigned)w->rec[j].prio;
+    } else {
+      e.tb = ~0ull;
+      e.prio = 0xffffffffu;
+    }
+    e.idx = (unsigned)j;
+  }
+  t_sync();
+  for (int kk = 2; kk <= np2; kk <<= 1) {
+    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+      for (int x = EC_LANE; x < np2; x += EC_TSIZE) {
+        int y = x ^ jj;
+        if (y > x) {
+          SortE ex = w->srt[x], ey = w->srt[y];
+          bool up = (x & kk) == 0;
+          bool gt = key_less(ey.tb, ey.prio, ex.tb, ex.prio);
+          if (gt == up) {
+            w->srt[x] = ey;
+            w->srt[y] = ex;
+          }
+        }
+      }
+      t_sync();
+    }
+  }
+  /* ---- 5. commit walk (lane 0) */
+  if (EC_LANE == 0) {
+    const AsbScenario& sc = w->sc;
+    int stop = STOP_NONE, stop_idx = -1;
+    int p = 0;
+    while (p < n && stop == STOP_NONE) {
+      const unsigned long long tb = w->srt[p].tb;
+      const unsigned pr = w->srt[p].prio;
+      if (!key_less(tb, pr, w->hz_t, (unsigned)w->hz_p) &&
+          !(tb == w->hz_t && pr == (unsigned)w->hz_p)) {
+        stop = STOP_HORIZON;
+        break;
+      }
+      int q = p + 1;
+      while (q < n && w->srt[q].tb == tb && w->srt[q].prio == pr) q++;
+      if (q - p > 1) {
+        /* tie group: order by push sequence (every parent is already walked) */
+        for (int x = p + 1; x < q; x++) {
+          SortE e = w->srt[x];
+          long long sq = w->rec[e.idx].seq;
+          int y = x - 1;
+          while (y >= p && w->rec[w->srt[y].idx].seq > sq) {
+            w->srt[y + 1] = w->srt[y];
+            y--;
+          }
+          w->srt[y + 1] = e;
+        }
+      }
+      for (int x = p; x < q; x++) {
+        const int ri = (int)w->srt[x].idx;
+        Rec& r = w->rec[ri];
+        if (!below_horizon(tb, pr, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+          stop = STOP_HORIZON;
+          break;
+        }
+        const double t = r.t;
+        if (r.prio == EV_COMPLETE) {
+          Inst& in = w->in[r.inst - 1];
+          long long nu = in.usage + r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
+          int flip = (nu > sc.capacity ? 1 : 0) != in.thr;
+          if (flip || sc.interference > 0) {
+            stop = STOP_COUPLING;
+            stop_idx = ri;
+            break;
+          }
+          in.running -= 1;
+          in.usage = nu;
+          w->ctr[ASB_CTR_TURNS]++;
+          w->ctr[ASB_CTR_EVENTS]++;
+          if (r.flags & F_LAST) {
+            w->ctr[ASB_CTR_COMPLETED]++;
+          } else {
+            r.push_seq = w->seq++;
+            if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
+          }
+          update_power(w, r.inst, t);
+        } else if (r.prio == EV_ARRIVAL) {
+          /* _on_arrival, engine.py:490-507 */
+          int a = r.agent;
+          int target = route_arrival(w);
+          Inst& dst = w->in[target - 1];
+          g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
+          dst.fifo_len++;
+          g.inst[a] = target;
+          g.sa[a] = 0;
+          g.phase[a] = ASB_PHASE_PENDING;
+          g.tp[a] = EC_INF;
+          g.rank[a] = w->arr_rank++;
+          g.alive[w->n_alive++] = a;
+          w->arr_ptr = (int)r.seq + 1;
+          w->ctr[ASB_CTR_ARRIVED]++;
+        } else {
+          /* EV_TOOL (maybe a reassignment check) or EV_ISSUE, then _start_turn */
+          if (((r.flags & F_CHECK) && reassign_target(w, r.inst)) || sc.interference > 0) {
+            stop = STOP_COUPLING;
+            stop_idx = ri;
+            break;
+          }
+          Inst& in = w->in[r.inst - 1];
+          if (in.log_len >= g.A) {
+            stop = STOP_LOGFULL;
+            stop_idx = ri;
+            break;
+          }
+          in.running += 1;
+          r.push_seq = w->seq++;
+          if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
+          r.aux64 = w->start_ctr++;
+          r.logpos = log_append(w, g, r.inst, r.agent);
+          w->ctr[ASB_CTR_EVENTS]++;
+          update_power(w, r.inst, t);
+        }
+        r.flags |= F_COMMITTED;
+      }
+      p = q;
+    }
+    /* something was dropped (buffer overflow): the window is not exhausted */
+    if (stop == STOP_NONE && w->hz_t != EC_INF_BITS) stop = STOP_HORIZON;
+    w->stop_kind = stop;
+    w->stop_rec = stop_idx;
+    if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
+  }
+  t_sync();
+  /* ---- 6. apply committed chain prefixes (lane per agent) */
+  for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
+    if (!(w->rec[d].flags & F_COMMITTED)) continue;
+    Cur c;
+    cur_load(g, c, w->due[d]);
+    int ri = d;
+    Rec tmp;
+    long long nseq = -1, srank = -1;
+    int lpos = -1;
+    while (ri >= 0 && (w->rec[ri].flags & F_COMMITTED)) {
+      const Rec& r = w->rec[ri];
+      cur_step(w, g, c, tmp, true);
+      nseq = r.push_seq;
+      if (r.prio != EV_COMPLETE) {
+        srank = r.aux64;
+        lpos = r.logpos;
+      }
+      ri = r.child;
+    }
+    const int a = c.a;
+    g.ctx[a] = c.ctx;
+    g.dec[a] = c.dec;
+    g.maxctx[a] = c.maxctx;
+    g.llm[a] = c.llm;
+    g.steps[a] = c.steps;
+    g.sa[a] = c.sa;
+    g.phase[a] = c.phase;
+    g.issue[a] = c.issue;
+    g.anchor[a] = c.anchor;
+    g.rem[a] = c.rem;
+    g.done[a] = c.done;
+    g.next_prio[a] = c.prio;
+    if (c.prio > 0) {
+      g.next_t[a] = c.t;
+      g.next_seq[a] = nseq;
+    }
+    if (srank >= 0) {
+      g.start_rank[a] = srank;
+      g.logpos[a] = lpos;
+    }
+    if (c.phase == ASB_PHASE_DONE) {
+      g.tp[a] = EC_NAN;
+      g.ctime[a] = c.t;
+    } else if (c.llm > 0.0) {
+      g.tp[a] = (double)c.dec / c.llm;
+    }
+  }
+  t_sync();
+  if (EC_LANE == 0) w->ctr[ASB_CTR_BATCHES]++;
+  /* ---- 7. coupling / overflow follow-ups */
+  const int stop = w->stop_kind;
+  if (stop == STOP_COUPLING) {
+    Rec r = w->stop_r;
+    exec_serial(w, g, r);
+    return BATCH_MORE;
+  }
+  if (stop == STOP_LOGFULL) {
+    log_pass(w, g, w->stop_r.inst, 0);
+    return BATCH_MORE;
+  }
+  if (stop == STOP_HORIZON) return BATCH_MORE;
+  if (bound != win_end || incl != w->incl) {
+    /* the shrunk window is fully committed: continue from its end */
+    if (EC_LANE == 0) w->now = bound;
+    t_sync();
+    return BATCH_MORE;
+  }
+  return BATCH_DONE;
+}
+
+/* exact single-event fallback: process the minimum pending event serially
+ * (used only when a burst of identical timestamps exceeds the batch buffers) */
+template <class W>
+EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
+  /* min over alive agents' next events by (t, prio, seq) */
+  unsigned long long bt = EC_INF_BITS;
+  unsigned bp = 0xffffffffu;
+  long long bs = 0x7fffffffffffffffll;
+  int ba = -1;
+  for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
+    int a = g.alive[j];
+    int pr = g.next_prio[a];
+    if (pr <= 0) continue;
+    unsigned long long tb = ec_bits(g.next_t[a]);
+    long long s = g.next_seq[a];
+    if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
+      bt = tb;
+      bp = (unsigned)pr;
+      bs = s;
+      ba = a;
+    }
+  }
+  for (int off = EC_TSIZE / 2; off > 0; off >>= 1) {
+    unsigned long long ot = t_shfl_xor_ull(bt, off);
+    unsigned op = (unsigned)t_shfl_xor_i((int)bp, off);
+    long long os = t_shfl_xor_ll(bs, off);
+    int oa = t_shfl_xor_i(ba, off);
+    if (key_less(ot, op, bt, bp) || (ot == bt && op == bp && os < bs)) {
+      bt = ot;
+      bp = op;
+      bs = os;
+      ba = oa;
+    }
+  }
+  /* pending arrival competes at priority 4 */
+  int arr = -1;
+  if (w->arr_ptr < g.A) {
+    int a = g.arr_order[w->arr_ptr];
+    double t = g.arrival[a];
+    if (t < w->sc.sim_duration && key_less(ec_bits(t), EV_ARRIVAL, bt, bp)) arr = a;
+  }
+  if (arr < 0 && ba < 0) return false;
+  double t = arr >= 0 ? g.arrival[arr] : ec_from_bits(bt);
+  if (!(w->incl ? t <= win_end : t < win_end)) return false;
+  if (arr >= 0) {
+    if (EC_LANE == 0) {
+      w->now = t;
+      int target = route_arrival(w);
+      Inst& dst = w->in[target - 1];
+      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = arr;
+      dst.fifo_len++;
+      g.inst[arr] = target;
+      g.sa[arr] = 0;
+      g.phase[arr] = ASB_PHASE_PENDING;
+      g.tp[arr] = EC_INF;
+      g.rank[arr] = w->arr_rank++;
+      g.alive[w->n_alive++] = arr;
+      w->arr_ptr++;
+      w->ctr[ASB_CTR_ARRIVED]++;
+    }
+    t_sync();
+    return true;
+  }
+  Rec r;
+  r.t = t;
+  r.prio = (short)bp;
+  r.agent = ba;
+  r.inst = g.inst[ba];
+  exec_serial(w, g, r);
+  return true;
+}
+
+template <class W, int RCAP, int DCAP, int ACAP>
+EC_DEV void run_scenario(W* w, const GP& g) {
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances, L = sc.n_levels, A = g.A;
+  /* ---- init (engine.py:251-276) */
+  for (int a = EC_LANE; a < A; a += EC_TSIZE) {
+    g.ctime[a] = EC_NAN;
+    g.llm[a] = 0.0;
+    g.tp[a] = EC_NAN;
+    g.issue[a] = 0.0;
+    g.anchor[a] = 0.0;
+    g.rem[a] = 0.0;
+    g.done[a] = 0.0;
+    g.next_t[a] = 0.0;
+    g.notbefore[a] = 0.0;
+    g.pissue[a] = EC_NAN;
+    g.dec[a] = 0;
+    g.maxctx[a] = 0;
+    g.ctx[a] = 0;
+    g.next_seq[a] = 0;
+    g.start_rank[a] = -1;
+    g.steps[a] = 0;
+    g.inst[a] = 0;
+    g.mig[a] = 0;
+    g.phase[a] = ASB_PHASE_ARRIVING;
+    g.rank[a] = -1;
+    g.next_prio[a] = 0;
+    g.sa[a] = 0;
+    g.logpos[a] = -1;
+  }
+  if (g.turn_issue) {
+    long long nt = g.aturn[A] - g.aturn[0];
+    for (long long t = EC_LANE; t < nt; t += EC_TSIZE) {
+      g.turn_issue[g.aturn[0] - g.turn_base + t] = EC_NAN;
+      g.turn_done[g.aturn[0] - g.turn_base + t] = EC_NAN;
+    }
+  }
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) {
+    Inst& in = w->in[i];
+    in.usage = 0;
+    in.watts = w->idle[L - 1];
+    in.t_pow = in.energy = in.thr_since = in.thr_time = 0.0;
+    in.level = L;
+    in.running = in.thr = in.thr_flag = 0;
+    in.key_valid = in.key_level = in.key_thr = in.key_run = 0;
+    in.fifo_head = in.fifo_len = in.log_len = 0;
+  }
+  if (EC_LANE == 0) {
+    w->now = 0.0;
+    w->seq = 0;
+    w->start_ctr = 0;
+    for (int c = 0; c < ASB_NCOUNTERS; c++) w->ctr[c] = 0;
+    w->n_alive = w->rr_next = w->arr_ptr = w->arr_rank = w->status = 0;
+  }
+  t_sync();
+  const long long K = sc.n_epochs;
+  const double E = sc.epoch_length, T = sc.sim_duration;
+  for (long long k = 0; k < K && w->status == 0; k++) {
+    if (EC_LANE == 0) w->now = (double)k * E;
+    t_sync();
+    epoch_event(w, g, k);
+    const bool last = k + 1 == K;
+    const double win_end = last ? T : (double)(k + 1) * E;
+    if (EC_LANE == 0) {
+      w->incl = last ? 1 : 0;
+      w->bound = win_end;
+    }
+    t_sync();
+    for (;;) {
+      if (w->status) break;
+      int rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);
+      if (rc == BATCH_MORE) continue;
+      if (rc == BATCH_DONE) break;
+      /* a same-timestamp burst larger than the due buffer: one exact step */
+      if (!serial_step(w, g, win_end)) break;
+    }
+  }
+  /* ---- final accounting (engine.py:595-603) and outputs */
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) {
+    Inst& in = w->in[i];
+    in.energy += in.watts * (T - in.t_pow);
+    in.t_pow = T;
+    if (in.thr_flag) {
+      in.thr_time += T - in.thr_since;
+      in.thr_since = T;
+    }
+    g.o_energy[i] = in.energy;
+    g.o_thr[i] = in.thr_time;
+    g.o_usage[i] = in.usage;
+    g.o_pending[i] = in.fifo_len;
+    g.o_level[i] = in.level;
+  }
+  t_sync();
+  if (EC_LANE == 0) {
+    w->ctr[ASB_CTR_STATUS] = w->status;
+    for (int c = 0; c < ASB_NCOUNTERS; c++) g.o_ctr[c] = w->ctr[c];
+  }
+  t_sync();
+}
+
+}  // namespace asb
+
+#endif
