@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""bench.py — agent-ticks/s of the batched scenario engine on B200.
+
+Workload (default, BASELINE.json configs[4] "C5"): the
+Monte-Carlo sweep sharded across GPUs — per GPU 512 scenarios = 64 seeds x 8
+cells {router context_aware|round_robin} x {controller context_aware|off} x
+{SLO tau 20|35}; each scenario 16 instances x ~10k agents (WorkloadSpec
+arrival_rate=10000/3600, 3600 s), 3600 control epochs.  Weak scaling: rank r
+simulates seeds [64r, 64r+64).  One step = every scenario of the shard run to
+completion (engine kernel + per-scenario stats + stats fold), plus the NCCL
+allreduce of the 8-double stats vector when N > 1.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+
+`--impl reference` times the CPU restatement of the reference (oracle/,
+serial C DES, OpenMP over scenarios on all host cores) on the same shard.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "agent-ticks/sec (batched scenarios)"
+UNIT = "agent-ticks/s"
+SEEDS_PER_GPU = 64
+HBM_FALLBACK = 6538.6
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    p.add_argument("--seeds-per-gpu", type=int, default=SEEDS_PER_GPU)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- workload
+
+
+def c5_cells():
+    import paper_2604_16682_b200 as asb
+
+    cells = []
+    for pol in ("context_aware", "round_robin"):
+        for var in ("context_aware", "off"):
+            for tau in (20.0, 35.0):
+                cells.append(asb.SimConfig(traces=[], instance_count=16, sim_duration=3600.0,
+                                           controller=asb.ControllerConfig(variant=var, slo_target=tau),
+                                           router=asb.RouterConfig(policy=pol)))
+    return cells
+
+
+def build_shard(rank: int, seeds_per_gpu: int):
+    import paper_2604_16682_b200 as asb
+    from paper_2604_16682_b200 import _abi, packing
+    from paper_2604_16682_b200.workload import generate_arrays
+
+    seeds = list(range(rank * seeds_per_gpu, (rank + 1) * seeds_per_gpu))
+    arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=s)) for s in seeds]
+    cells = c5_cells()
+    recs = [packing.scenario_record(c, t, 0) for t in range(len(seeds)) for c in cells]
+    scen = np.array(recs, dtype=_abi.SCENARIO_DTYPE)
+    batch = packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables([asb.default_frequency_table()]))
+    return batch, seeds
+
+
+def alg_bytes(batch, counters) -> float:
+    """B_alg = 20 N_ticks + 112 N_turns + 128 N_instance_epochs."""
+    from paper_2604_16682_b200 import _abi
+
+    ctr = counters.reshape(-1, _abi.ASB_NCOUNTERS)
+    ticks = float(ctr[:, _abi.CTR["ticks"]].sum())
+    turns = float(ctr[:, _abi.CTR["turns"]].sum())
+    inst_epochs = float((batch.scen["n_instances"].astype(np.int64) * batch.scen["n_epochs"]).sum())
+    return 20.0 * ticks + 112.0 * turns + 128.0 * inst_epochs
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK, "fallback (SURVEY/BASELINE measured copy bandwidth)"
+
+
+def ncu_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_engine_traffic.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_launch"), d
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU legs
+
+
+def cpu_run(batch, threads: int = 0):
+    from oracle.oracle import run_oracle
+
+    timing = {}
+    host, stats = run_oracle(batch, decisions=False, turn_log=False, threads=threads, timing=timing)
+    return host, stats, timing["seconds"]
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def reference_arm(args, world, rank):
+    """`--impl reference`: the CPU restatement of the reference on all host cores."""
+    if rank != 0:
+        return
+    from paper_2604_16682_b200 import _abi, _build
+
+    _build.build_oracle()
+    batch, seeds = build_shard(0, args.seeds_per_gpu)
+    cores = cpu_cores()
+    for _ in range(args.warmup):
+        cpu_run(batch, cores)
+    times, ticks = [], 0.0
+    for _ in range(args.steps):
+        host, _, sec = cpu_run(batch, cores)
+        times.append(sec)
+        ticks = float(host["counters"].reshape(-1, _abi.ASB_NCOUNTERS)[:, _abi.CTR["ticks"]].sum())
+    sec = sum(times) / len(times)
+    # the whole job at N GPUs is N shards; the CPU arm times one shard per step
+    value = ticks / sec
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(batch, seeds, world, "cpu"),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"one C5 shard per step: {batch.n} scenarios (seeds {seeds[0]}-{seeds[-1]} x 8 cells)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_block(batch, seeds, world, parallel):
+    from paper_2604_16682_b200 import _abi  # noqa: F401
+
+    n_agents = batch.total_agents / max(batch.n, 1)
+    tbytes = sum(getattr(batch.traces, k).nbytes for k in ("arrival", "agent_turn_off", "prefill", "decode", "tool"))
+    return {
+        "workload": "C5 Monte-Carlo sweep shard: 512 scenarios/GPU (64 seeds x 8 cells {ctx-aware,round-robin} "
+                    "router x {ctx-aware,off} controller x tau {20,35}), 16 instances x ~10k agents, 3600 s",
+        "scenarios_per_gpu": batch.n, "seeds_per_gpu": len(seeds), "instances": 16,
+        "mean_agents_per_scenario": round(n_agents, 1), "sim_duration_s": 3600.0, "epochs": 3600,
+        "parallelism": f"scenario-sharded x{world} ({parallel})",
+        "l2": f"inputs larger than L2: {tbytes / 2**20:.0f} MiB trace pool + workspace per GPU, no flush",
+    }
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        reference_arm(args, world, rank)
+        return
+    import torch
+
+    from paper_2604_16682_b200 import _abi, _build
+    from paper_2604_16682_b200.engine import DeviceBatch
+
+    _build.build_cuda()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    batch, seeds = build_shard(rank, args.seeds_per_gpu)
+    db = DeviceBatch(batch, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev0=None, ev1=None):
+        if ev0 is not None:
+            ev0.record(stream)
+        torch.ops.agentsim_b200.run_scenarios(db.scen, db.traces, db.tables, db.out_list, db.workspace,
+                                              batch.max_instances, batch.total_agents, batch.total_ring)
+        if ev1 is not None:
+            ev1.record(stream)
+        torch.ops.agentsim_b200.scenario_stats(db.scen, db.out_list, db.stats)
+        torch.ops.agentsim_b200.reduce_stats(db.stats, db.outputs["counters"], batch.n, db.red)
+        if pg is not None:
+            pg.all_reduce(db.red)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize(dev)
+    if pg is not None:
+        pg.barrier()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for k in range(args.steps):
+            step(*evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+    if pg is not None:
+        pg.barrier()
+    total_ms = t0.elapsed_time(t1)
+    kern_ms = [a.elapsed_time(b) for a, b in evs]
+    host_ctr = db.outputs["counters"].cpu().numpy()
+    red = db.red.cpu().numpy()
+    ticks_local = float(host_ctr.reshape(-1, _abi.ASB_NCOUNTERS)[:, _abi.CTR["ticks"]].sum())
+    ms_per_step = total_ms / args.steps
+    if pg is not None:
+        t = torch.tensor([ms_per_step, ticks_local], dtype=torch.float64, device=dev)
+        mx = t.clone()
+        pg.all_reduce(mx, op=pg.ReduceOp.MAX)
+        pg.all_reduce(t)
+        ms_max, ticks_all = float(mx[0]), float(t[1])
+    else:
+        ms_max, ticks_all = ms_per_step, ticks_local
+    value = ticks_all / (ms_max / 1e3)
+
+    # roofline of the dominant kernel (the engine) from its own CUDA events
+    b_alg = alg_bytes(batch, host_ctr)
+    kern_s = (sum(kern_ms) / len(kern_ms)) / 1e3
+    achieved = b_alg / kern_s / 1e9
+    peak, peak_src = hbm_peak()
+    traffic, _ = ncu_traffic()
+
+    # end-to-end through the public API with host buffers (pinned H2D + D2H of results)
+    e2e = None
+    if not args.no_e2e:
+        host_in = [torch.from_numpy(np.ascontiguousarray(batch.scen.view(np.uint8))).pin_memory()]
+        host_in += [torch.from_numpy(np.ascontiguousarray(getattr(batch.traces, k))).pin_memory()
+                    for k in _abi.TRACE_FIELDS]
+        host_in += [torch.from_numpy(np.ascontiguousarray(getattr(batch.tables, k))).pin_memory()
+                    for k in _abi.TABLE_FIELDS]
+        dev_in = [db.scen, *db.traces, *db.tables]
+        h2d = sum(t.numel() * t.element_size() for t in host_in)
+        out_stats = torch.empty(db.stats.shape, dtype=db.stats.dtype).pin_memory()
+        out_red = torch.empty(db.red.shape, dtype=db.red.dtype).pin_memory()
+        d2h = out_stats.numel() + out_red.numel() * 8
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        if pg is not None:
+            pg.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            for d_t, h_t in zip(dev_in, host_in):
+                d_t.copy_(h_t, non_blocking=True)
+            step()
+            out_stats.copy_(db.stats, non_blocking=True)
+            out_red.copy_(db.red, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        if pg is not None:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e2e_ms = float(t[0])
+        e2e = {"value": ticks_all / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms}
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        _build.build_oracle()
+        cores = cpu_cores()
+        host_ref, stats_ref, sec = cpu_run(batch, cores)
+        ctr_ref = host_ref["counters"].reshape(-1, _abi.ASB_NCOUNTERS)
+        cpu = {"value": float(ctr_ref[:, _abi.CTR["ticks"]].sum()) / sec, "unit": UNIT, "cores": cores,
+               "kind": "port",
+               "sample": f"the full shard ({batch.n} scenarios, {sec:.1f} s wall on {cores} threads): serial C "
+                         "restatement of the reference DES (oracle/des_oracle.c), OpenMP over scenarios"}
+        got = {k: t.cpu().numpy() for k, t in db.outputs.items()}
+        keys = [k for k in _abi.AGENT_OUT] + [k for k in _abi.INST_OUT]
+        same = all(np.array_equal(got[k], host_ref[k], equal_nan=got[k].dtype.kind == "f") for k in keys)
+        a = got["counters"].reshape(-1, _abi.ASB_NCOUNTERS)[:, :9]
+        same = same and np.array_equal(a, ctr_ref[:, :9])
+        parity = f"{'bit-exact' if same else 'MISMATCH'} vs oracle on all {batch.n} scenarios of the timed shard"
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (vectorised generator, reference distributions)",
+            "config": config_block(batch, seeds, world, "nccl allreduce of stats" if world > 1 else "1 GPU"),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "asb_engine_kernel", "kernel_ms": kern_s * 1e3,
+                         "alg_bytes_per_launch": b_alg, "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": 4 * args.steps,
+            "parity": parity,
+            "stats": {k: float(v) for k, v in zip(_abi.RED, red)},
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,38 @@
+"""The C-ABI library loads (no GPU needed) and exports every symbol the
+header declares; the ctypes/numpy mirrors match the C struct layouts."""
+
+import ctypes
+import os
+import re
+
+from common import ROOT
+from paper_2604_16682_b200 import _abi, _build, _native
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "agentsim_b200.h")).read()
+    return sorted(set(re.findall(r"^(?:int|size_t)\s+(asb_\w+)\(", text, flags=re.M)))
+
+
+def test_library_builds_and_exports_every_declared_symbol():
+    _build.build_cuda()
+    lib = _native.lib()
+    names = header_functions()
+    assert len(names) >= 10
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_struct_layouts_match_header():
+    lib = _native.lib()
+    buf = (ctypes.c_int64 * 6)()
+    assert lib.asb_struct_sizes(buf) == 6
+    assert list(buf) == _abi.struct_sizes()
+    assert lib.asb_abi_version() == 1
+
+
+def test_workspace_size_is_monotone():
+    lib = _native.lib()
+    a = lib.asb_workspace_bytes(4, 1000, 16000)
+    b = lib.asb_workspace_bytes(4, 2000, 32000)
+    assert 0 < a < b

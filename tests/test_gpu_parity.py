@@ -1,0 +1,131 @@
+"""GPU parity: the sm_100a engine through the C ABI against the reference's
+golden vectors and the (pinned) oracle — bit-exact for every integer,
+index and decision field, and (stricter than the 1e-5 contract) for the
+floats too."""
+
+import glob
+import os
+import random
+
+import numpy as np
+import pytest
+
+import paper_2604_16682_b200 as asb
+from common import (GOLDEN, array_outputs_equal, canonical, config_from_dict, digest, first_difference,
+                    load_golden, traces_from_json, traces_to_json)
+from oracle.oracle import run_oracle
+from paper_2604_16682_b200 import _abi, packing
+from paper_2604_16682_b200.engine import DeviceBatch, build_results, prepare_batch
+from paper_2604_16682_b200.workload import generate_arrays
+
+pytestmark = pytest.mark.gpu
+
+FULL = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "*.json.gz"))
+              if not os.path.basename(p).startswith(("c3", "c4", "c5")))
+DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz")))
+
+
+def gpu(batch, decisions=True, turn_log=True):
+    dev = DeviceBatch(batch, device="cuda:0", decisions=decisions, turn_log=turn_log)
+    dev.run()
+    return dev.download()
+
+
+def test_golden_full_cases_in_one_batch(cuda_device):
+    goldens = [load_golden(n) for n in FULL]
+    cfgs = [config_from_dict(asb, g["config"], traces_from_json(asb, g["trace"])) for g in goldens]
+    batch = prepare_batch(cfgs)
+    host, stats = gpu(batch)
+    results = build_results(batch, host, stats, cfgs, None)
+    for g, r in zip(goldens, results):
+        diff = first_difference(g["expected"], canonical(r))
+        assert diff is None, (g["name"], diff)
+        assert r.counters["ticks"] == g["ticks"], g["name"]
+
+
+@pytest.mark.parametrize("name", DIGEST)
+def test_golden_config_digests(cuda_device, name):
+    g = load_golden(name)
+    traces = asb.generate_workload(asb.WorkloadSpec(**g["spec"]))
+    if digest(traces_to_json(traces)) != g["trace_digest"]:
+        pytest.skip("numpy RNG stream differs from the golden trace's")
+    cfg = config_from_dict(asb, g["config"], traces)
+    batch = prepare_batch([cfg])
+    host, stats = gpu(batch)
+    (r,) = build_results(batch, host, stats, [cfg], None)
+    can = canonical(r)
+    bad = [k for k in g["digests"] if digest(can[k]) != g["digests"][k]]
+    assert not bad, (bad, can["system"], g["summary"]["system"])
+    assert r.counters["ticks"] == g["ticks"]
+
+
+def _random_configs(seed, n):
+    from test_host_engine import random_configs
+
+    return random_configs(seed, n)
+
+
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_random_batch_matches_oracle(cuda_device, seed):
+    batch = prepare_batch(_random_configs(seed, 96))
+    got, gst = gpu(batch)
+    want, wst = run_oracle(batch)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
+    for f in _abi.STATS_DTYPE.names:
+        assert np.array_equal(gst[f], wst[f], equal_nan=True), f
+
+
+def c5_batch(seeds, cells=None):
+    arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=s)) for s in seeds]
+    cfgs = []
+    for pol in ("context_aware", "round_robin"):
+        for var in ("context_aware", "off"):
+            for tau in (20.0, 35.0):
+                cfgs.append(asb.SimConfig(traces=[], instance_count=16, sim_duration=3600.0,
+                                          controller=asb.ControllerConfig(variant=var, slo_target=tau),
+                                          router=asb.RouterConfig(policy=pol)))
+    cfgs = cfgs if cells is None else [cfgs[c] for c in cells]
+    recs = [packing.scenario_record(c, t, 0) for t in range(len(seeds)) for c in cfgs]
+    scen = np.array(recs, dtype=_abi.SCENARIO_DTYPE)
+    return packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables([asb.default_frequency_table()]))
+
+
+def test_c5_full_size_scenarios_match_oracle(cuda_device):
+    """Full-size C5 scenarios (16 instances x ~10k agents x 3600 epochs), all 8 cells."""
+    batch = c5_batch([101, 102, 103, 104])
+    got, gst = gpu(batch, decisions=True, turn_log=False)
+    want, wst = run_oracle(batch, decisions=True, turn_log=False)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
+    ctr = got["counters"].reshape(-1, _abi.ASB_NCOUNTERS)
+    assert (ctr[:, _abi.CTR["ticks"]] > 5_000_000).all()
+
+
+def test_c5_size_independent_properties(cuda_device):
+    """Conservation laws at full size: final instance usage equals the summed
+    context of the agents still resident on it; agent-ticks equal the closed
+    form of SURVEY §0; completed agents consumed all their turns."""
+    batch = c5_batch([7, 8], cells=[0, 3, 5, 6])
+    host, _ = gpu(batch, decisions=False, turn_log=False)
+    ctr = host["counters"].reshape(-1, _abi.ASB_NCOUNTERS)
+    tp = batch.traces
+    for s in range(batch.n):
+        a0, a1 = batch.agent_off[s], batch.agent_off[s + 1]
+        t = int(batch.scen[s]["trace_id"])
+        g0 = tp.trace_agent_off[t]
+        phase = host["phase"][a0:a1]
+        inst = host["final_instance"][a0:a1]
+        ctx = host["context"][a0:a1]
+        resident = np.isin(phase, [2, 3, 4])
+        m = int(batch.scen[s]["n_instances"])
+        usage = np.bincount(inst[resident], weights=ctx[resident], minlength=m + 1)[1:]
+        assert np.array_equal(usage.astype(np.int64), host["final_usage"][batch.inst_off[s]: batch.inst_off[s + 1]])
+        n_turns = tp.agent_turn_off[g0 + 1: g0 + (a1 - a0) + 1] - tp.agent_turn_off[g0: g0 + (a1 - a0)]
+        done = phase == 5
+        assert np.array_equal(host["turns_completed"][a0:a1][done], n_turns[done])
+        arr = tp.arrival[g0: g0 + (a1 - a0)]
+        comp = host["completion_time"][a0:a1]
+        arrived = host["arrival_rank"][a0:a1] >= 0
+        want = asb.engine.agent_ticks_closed_form(arr[arrived], comp[arrived], 1.0, int(batch.scen[s]["n_epochs"]))
+        assert ctr[s, _abi.CTR["ticks"]] == want

@@ -1,0 +1,51 @@
+"""Pin the C oracle to golden vectors produced by the reference itself
+(tests/golden/make_golden.py): every known-answer case of the reference's
+test_engine.py, 24 random configurations, tie storms, and the BASELINE
+configurations C1-C5 (full results for C1/C2, SHA-256 digests for the
+larger ones).  Exact equality, floats included."""
+
+import glob
+import os
+
+import pytest
+
+import paper_2604_16682_b200 as asb
+from common import (GOLDEN, canonical, config_from_dict, digest, first_difference, load_golden, results_via,
+                    traces_from_json, traces_to_json)
+from oracle.oracle import run_oracle
+
+FULL = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "*.json.gz"))
+              if not os.path.basename(p).startswith(("c3", "c4", "c5")))
+DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz")))
+
+
+def golden_config(g):
+    if "trace" in g:
+        traces = traces_from_json(asb, g["trace"])
+    else:
+        traces = asb.generate_workload(asb.WorkloadSpec(**g["spec"]))
+        if digest(traces_to_json(traces)) != g["trace_digest"]:
+            pytest.skip("numpy RNG stream differs from the one that generated the golden trace")
+    return config_from_dict(asb, g["config"], traces)
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_oracle_matches_reference_full(name):
+    g = load_golden(name)
+    cfg = golden_config(g)
+    (res,), host = results_via(run_oracle, [cfg])
+    diff = first_difference(g["expected"], canonical(res))
+    assert diff is None, diff
+    assert res.counters["ticks"] == g["ticks"]
+
+
+@pytest.mark.parametrize("name", DIGEST)
+def test_oracle_matches_reference_digest(name):
+    g = load_golden(name)
+    cfg = golden_config(g)
+    (res,), host = results_via(run_oracle, [cfg])
+    can = canonical(res)
+    got = {k: digest(v) for k, v in can.items()}
+    bad = [k for k in g["digests"] if got[k] != g["digests"][k]]
+    assert not bad, (bad, can["system"], g["summary"]["system"])
+    assert res.counters["ticks"] == g["ticks"]
