@@ -19,6 +19,7 @@ PKG = os.path.join(ROOT, "paper_2604_16682_b200")
 CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200.so")
+PROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_prof.so")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "build", "liboracle.so")
 HOST_ENGINE_LIB = os.path.join(ROOT, "tests", "native", "build", "libhost_engine.so")
 
@@ -47,17 +48,22 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
 
 
-def build_cuda(force: bool = False, verbose: bool = False) -> str:
+def build_cuda(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """The product library; ``profile=True`` builds the phase-timing variant
+    (-DASB_PROFILE, counters[10..15]) used only by tools/profile_phases.py."""
     srcs = [os.path.join(CSRC, f) for f in ("engine.cu", "unit_ops.cu")]
     deps = srcs + [os.path.join(CSRC, "engine_core.h"), os.path.join(ROOT, "include", "agentsim_b200.h")]
-    if force or _stale(LIB_PATH, deps):
+    target = PROF_LIB_PATH if profile else LIB_PATH
+    if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
-        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", LIB_PATH + ".tmp", *srcs]
+        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", target + ".tmp", *srcs]
+        if profile:
+            cmd.insert(1, "-DASB_PROFILE")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
-        os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+        os.replace(target + ".tmp", target)
+    return target
 
 
 def build_oracle(force: bool = False) -> str:
@@ -84,6 +90,7 @@ def build_host_engine(force: bool = False) -> str:
 
 def build_all(force: bool = False) -> None:
     build_cuda(force)
+    build_cuda(force, profile=True)
     build_oracle(force)
     build_host_engine(force)
 

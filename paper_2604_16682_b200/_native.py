@@ -45,12 +45,13 @@ def lib() -> C.CDLL:
     """The loaded CUDA library (raises NativeUnavailable when not built)."""
     global _LIB
     if _LIB is None:
-        if not os.path.exists(LIB_PATH):
+        path = os.environ.get("ASB_LIB", LIB_PATH)
+        if not os.path.exists(path):
             raise NativeUnavailable(
-                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "(the B200 engine has no CPU fallback)"
             )
-        handle = C.CDLL(LIB_PATH)
+        handle = C.CDLL(path)
         _declare(handle)
         _LIB = handle
     return _LIB

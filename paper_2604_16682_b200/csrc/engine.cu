@@ -55,6 +55,7 @@ EC_DEV bool ec_isnan(double x) { return isnan(x); }
 EC_DEV double ec_floor(double x) { return floor(x); }
 EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__double_as_longlong(x); }
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
+EC_DEV long long ec_clock() { return clock64(); }
 
 #include "engine_core.h"
 

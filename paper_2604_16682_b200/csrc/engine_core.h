@@ -47,6 +47,10 @@
  *   ec_floor(x), EC_NAN, EC_INF
  */
 
+#ifndef EC_DEPCAP
+#define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
+#endif
+
 namespace asb {
 
 enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4 };
@@ -129,7 +133,35 @@ struct WS {
   Rec rec[RCAP];
   SortE srt[RCAP];
   Rec stop_r;
+  int depk[RCAP];
+  long long snap[EC_DEPCAP][MAXM];
+  long long prof[6];
+  long long prof_t;
 };
+
+/* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
+ * accumulated by lane 0 and reported in counters[10..15] */
+#ifdef ASB_PROFILE
+#define EC_PROF_START(w) \
+  do {                   \
+    if (EC_LANE == 0) (w)->prof_t = ec_clock(); \
+  } while (0)
+#define EC_PROF(w, k)                                  \
+  do {                                                 \
+    if (EC_LANE == 0) {                                \
+      long long now_ = ec_clock();                     \
+      (w)->prof[k] += now_ - (w)->prof_t;              \
+      (w)->prof_t = now_;                              \
+    }                                                  \
+  } while (0)
+#else
+#define EC_PROF_START(w) \
+  do {                   \
+  } while (0)
+#define EC_PROF(w, k) \
+  do {                \
+  } while (0)
+#endif
 
 /* ----------------------------------------------------------------------------
  * small scalar helpers (any lane)
@@ -551,32 +583,52 @@ EC_DEV bool is_due(const W* w, double t) {
   return w->incl ? (t <= w->bound) : (t < w->bound);
 }
 
+/* unroll depth of the alive-list sweeps: independent gathers in flight per lane */
+#ifndef EC_SWEEP_UNROLL
+#define EC_SWEEP_UNROLL 8
+#endif
+
 /* agent-tick sweep: per-instance count and min running throughput over the
  * alive list (ongoing ∪ pending of every instance), with lazy compaction of
  * finished agents.  controller.py:89-103, engine.py:437-454 (team) */
 template <class W>
 EC_DEV void tick_sweep(W* w, const GP& g) {
+  constexpr int U = EC_SWEEP_UNROLL;
   const int M = w->sc.n_instances;
   for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS;
   t_sync();
   const int n = w->n_alive;
   int cur_i = 0, dead = 0;
   unsigned long long cur_m = EC_INF_BITS;
-  for (int j = EC_LANE; j < n; j += EC_TSIZE) {
-    int a = g.alive[j];
-    double tp = g.tp[a];
-    if (ec_isnan(tp)) {
-      dead++;
-      continue;
+  for (int base = 0; base < n; base += EC_TSIZE * U) {
+    int a[U];
+    double tp[U];
+    int ii[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int j = base + u * EC_TSIZE + EC_LANE;
+      a[u] = j < n ? g.alive[j] : -1;
     }
-    int i = g.inst[a];
-    if (i != cur_i) {
-      if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
-      cur_i = i;
-      cur_m = EC_INF_BITS;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      tp[u] = a[u] >= 0 ? g.tp[a[u]] : EC_NAN;
+      ii[u] = a[u] >= 0 ? g.inst[a[u]] : 0;
     }
-    unsigned long long b = ec_bits(tp);
-    if (b < cur_m) cur_m = b;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (a[u] < 0) continue;
+      if (ec_isnan(tp[u])) {
+        dead++;
+        continue;
+      }
+      if (ii[u] != cur_i) {
+        if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
+        cur_i = ii[u];
+        cur_m = EC_INF_BITS;
+      }
+      unsigned long long b = ec_bits(tp[u]);
+      if (b < cur_m) cur_m = b;
+    }
   }
   if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
   long long dead_all = t_sum_ll(dead);
@@ -638,7 +690,9 @@ template <class W>
 EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances, L = sc.n_levels;
+  EC_PROF_START(w);
   tick_sweep(w, g);
+  EC_PROF(w, 0);
   for (int i = 1; i <= M; i++) {
     Inst& in = w->in[i - 1];
     const long long usage_obs = in.usage;
@@ -767,20 +821,66 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
     }
     t_sync();
   }
+  EC_PROF(w, 1);
 }
 
 /* count alive agents whose next event is due before `bound` (team) */
 template <class W>
 EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
+  constexpr int U = EC_SWEEP_UNROLL;
   int c = 0;
-  for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
-    int a = g.alive[j];
-    if (g.next_prio[a] > 0) {
-      double t = g.next_t[a];
-      if (incl ? t <= bound : t < bound) c++;
+  const int n = w->n_alive;
+  for (int base = 0; base < n; base += EC_TSIZE * U) {
+    int a[U], pr[U];
+    double t[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int j = base + u * EC_TSIZE + EC_LANE;
+      a[u] = j < n ? g.alive[j] : -1;
     }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      pr[u] = a[u] >= 0 ? g.next_prio[a[u]] : 0;
+      t[u] = a[u] >= 0 ? g.next_t[a[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++)
+      if (pr[u] > 0 && (incl ? t[u] <= bound : t[u] < bound)) c++;
   }
   return (int)t_sum_ll(c);
+}
+
+/* one pass: collect due agents into w->due (up to DCAP); returns the total
+ * due count (> DCAP means the list is incomplete) (team) */
+template <class W, int DCAP>
+EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
+  constexpr int U = EC_SWEEP_UNROLL;
+  const int n = w->n_alive;
+  int total = 0;
+  for (int base = 0; base < n; base += EC_TSIZE * U) {
+    int a[U], pr[U];
+    double t[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      int j = base + u * EC_TSIZE + EC_LANE;
+      a[u] = j < n ? g.alive[j] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      pr[u] = a[u] >= 0 ? g.next_prio[a[u]] : 0;
+      t[u] = a[u] >= 0 ? g.next_t[a[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      bool due = pr[u] > 0 && (incl ? t[u] <= bound : t[u] < bound);
+      unsigned m = t_ballot(due);
+      int pos = total + ec_popc(m & t_lt_mask());
+      if (due && pos < DCAP) w->due[pos] = a[u];
+      total += ec_popc(m);
+    }
+  }
+  t_sync();
+  return total;
 }
 
 /* horizon key: records are committed only while (t, prio, seq) < (hz_t, hz_p, hz_s) */
@@ -793,13 +893,382 @@ EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, uns
 
 enum { BATCH_DONE = 0, BATCH_MORE = 1, BATCH_SERIAL = 2 };
 
+/* Serial commit walk (lane 0): the reference's handlers in (time, prio, seq)
+ * order, stopping before the first coupling event.  Used for interference
+ * mode and for tie groups whose push order is not resolved yet. */
+template <class W>
+EC_DEV void walk_serial(W* w, const GP& g, const int n) {
+  if (EC_LANE == 0) {
+    const AsbScenario& sc = w->sc;
+    int stop = STOP_NONE, stop_idx = -1;
+    int p = 0;
+    while (p < n && stop == STOP_NONE) {
+      const unsigned long long tb = w->srt[p].tb;
+      const unsigned pr = w->srt[p].prio;
+      if (!key_less(tb, pr, w->hz_t, (unsigned)w->hz_p) &&
+          !(tb == w->hz_t && pr == (unsigned)w->hz_p)) {
+        stop = STOP_HORIZON;
+        break;
+      }
+      int q = p + 1;
+      while (q < n && w->srt[q].tb == tb && w->srt[q].prio == pr) q++;
+      if (q - p > 1) {
+        /* tie group: order by push sequence (every parent is already walked) */
+        for (int x = p + 1; x < q; x++) {
+          SortE e = w->srt[x];
+          long long sq = w->rec[e.idx].seq;
+          int y = x - 1;
+          while (y >= p && w->rec[w->srt[y].idx].seq > sq) {
+            w->srt[y + 1] = w->srt[y];
+            y--;
+          }
+          w->srt[y + 1] = e;
+        }
+      }
+      for (int x = p; x < q; x++) {
+        const int ri = (int)w->srt[x].idx;
+        Rec& r = w->rec[ri];
+        if (!below_horizon(tb, pr, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+          stop = STOP_HORIZON;
+          break;
+        }
+        const double t = r.t;
+        if (r.prio == EV_COMPLETE) {
+          Inst& in = w->in[r.inst - 1];
+          long long nu = in.usage + r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
+          int flip = (nu > sc.capacity ? 1 : 0) != in.thr;
+          if (flip || sc.interference > 0) {
+            stop = STOP_COUPLING;
+            stop_idx = ri;
+            break;
+          }
+          in.running -= 1;
+          in.usage = nu;
+          w->ctr[ASB_CTR_TURNS]++;
+          w->ctr[ASB_CTR_EVENTS]++;
+          if (r.flags & F_LAST) {
+            w->ctr[ASB_CTR_COMPLETED]++;
+          } else {
+            r.push_seq = w->seq++;
+            if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
+          }
+          update_power(w, r.inst, t);
+        } else if (r.prio == EV_ARRIVAL) {
+          /* _on_arrival, engine.py:490-507 */
+          int a = r.agent;
+          int target = route_arrival(w);
+          Inst& dst = w->in[target - 1];
+          g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
+          dst.fifo_len++;
+          g.inst[a] = target;
+          g.sa[a] = 0;
+          g.phase[a] = ASB_PHASE_PENDING;
+          g.tp[a] = EC_INF;
+          g.rank[a] = w->arr_rank++;
+          g.alive[w->n_alive++] = a;
+          w->arr_ptr = (int)r.seq + 1;
+          w->ctr[ASB_CTR_ARRIVED]++;
+        } else {
+          /* EV_TOOL (maybe a reassignment check) or EV_ISSUE, then _start_turn */
+          if (((r.flags & F_CHECK) && reassign_target(w, r.inst)) || sc.interference > 0) {
+            stop = STOP_COUPLING;
+            stop_idx = ri;
+            break;
+          }
+          Inst& in = w->in[r.inst - 1];
+          if (in.log_len >= g.A) {
+            stop = STOP_LOGFULL;
+            stop_idx = ri;
+            break;
+          }
+          in.running += 1;
+          r.push_seq = w->seq++;
+          if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
+          r.aux64 = w->start_ctr++;
+          r.logpos = log_append(w, g, r.inst, r.agent);
+          w->ctr[ASB_CTR_EVENTS]++;
+          update_power(w, r.inst, t);
+        }
+        r.flags |= F_COMMITTED;
+      }
+      p = q;
+    }
+    /* something was dropped (buffer overflow): the window is not exhausted */
+    if (stop == STOP_NONE && w->hz_t != EC_INF_BITS) stop = STOP_HORIZON;
+    w->stop_kind = stop;
+    w->stop_rec = stop_idx;
+    if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
+  }
+  t_sync();
+}
+
+
+/* Parallel commit walk (team).  The serial walk's state machine decomposes
+ * by instance: usage, running count, thrash flag, power and the running log
+ * of instance i change only at records on i.  Each lane owns instances and
+ * replays their records in walk order (finding the first thrash flip / log
+ * overflow), usage snapshots are taken at the records that read all
+ * instances (arrivals, reassignment checks), and push sequence numbers /
+ * start ranks are warp prefix scans.  Returns false (caller falls back to
+ * walk_serial) under interference or when a tie group contains a record
+ * whose push order is only known during the walk. */
+template <class W, int RCAP>
+EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
+  const AsbScenario& sc = w->sc;
+  if (sc.interference > 0) return false;
+  const int M = sc.n_instances;
+  /* ---- step 0: tie groups, horizon cut, dependent-record numbering */
+  int tie = 0, unknown = 0;
+  for (int p = EC_LANE; p + 1 < n; p += EC_TSIZE) {
+    const SortE& e0 = w->srt[p];
+    const SortE& e1 = w->srt[p + 1];
+    if (e0.tb == e1.tb && e0.prio == e1.prio) {
+      tie = 1;
+      if (w->rec[e0.idx].seq < 0 || w->rec[e1.idx].seq < 0) unknown = 1;
+    }
+  }
+  if (t_sum_ll(unknown)) return false;
+  if (t_sum_ll(tie)) {
+    if (EC_LANE == 0) {
+      for (int p = 0; p < n;) {
+        int q = p + 1;
+        while (q < n && w->srt[q].tb == w->srt[p].tb && w->srt[q].prio == w->srt[p].prio) q++;
+        for (int x = p + 1; x < q; x++) {
+          SortE e = w->srt[x];
+          long long sq = w->rec[e.idx].seq;
+          int y = x - 1;
+          while (y >= p && w->rec[w->srt[y].idx].seq > sq) {
+            w->srt[y + 1] = w->srt[y];
+            y--;
+          }
+          w->srt[y + 1] = e;
+        }
+        p = q;
+      }
+    }
+    t_sync();
+  }
+  int cut = n;
+  int ndep = 0;
+  for (int base = 0; base < n; base += EC_TSIZE) {
+    const int p = base + EC_LANE;
+    bool dep = false;
+    if (p < n) {
+      const SortE& e = w->srt[p];
+      const Rec& r = w->rec[e.idx];
+      if (!below_horizon(e.tb, e.prio, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s) && p < cut) cut = p;
+      dep = r.prio == EV_ARRIVAL || (r.prio == EV_TOOL && (r.flags & F_CHECK));
+    }
+    unsigned m = t_ballot(dep);
+    int k = ndep + ec_popc(m & t_lt_mask());
+    if (p < n) {
+      w->depk[p] = dep ? k : -1;
+      if (dep && k == EC_DEPCAP && p < cut) cut = p; /* snapshot table full: stop before it */
+    }
+    ndep += ec_popc(m);
+  }
+  for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
+    int oc = t_shfl_xor_i(cut, o);
+    cut = oc < cut ? oc : cut;
+  }
+  t_sync();
+  /* ---- step 1: per-instance replay up to the cut: first flip / log overflow, snapshots */
+  int first = cut;
+  int first_lf = cut;
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    const Inst& in = w->in[i - 1];
+    long long u = in.usage;
+    const int thr = in.thr;
+    int lg = in.log_len;
+    for (int p = 0; p < cut; p++) {
+      const int k = w->depk[p];
+      if (k >= 0) w->snap[k][i - 1] = u;
+      const Rec& r = w->rec[w->srt[p].idx];
+      if (r.inst != i) continue;
+      if (r.prio == EV_COMPLETE) {
+        long long nu = u + r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
+        if ((nu > sc.capacity ? 1 : 0) != thr) {
+          if (p < first) first = p;
+          break;
+        }
+        u = nu;
+      } else if (r.prio != EV_ARRIVAL) {
+        if (lg >= g.A) {
+          if (p < first_lf) first_lf = p;
+          break;
+        }
+        lg++;
+      }
+    }
+  }
+  for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
+    int a = t_shfl_xor_i(first, o), b = t_shfl_xor_i(first_lf, o);
+    first = a < first ? a : first;
+    first_lf = b < first_lf ? b : first_lf;
+  }
+  t_sync();
+  /* ---- step 2: reassignment checks in order (team argmin on the snapshot) */
+  int stop_p = first < first_lf ? first : first_lf;
+  int stop_kind = stop_p == cut ? STOP_NONE : (first <= first_lf ? STOP_COUPLING : STOP_LOGFULL);
+  for (int p = 0; p < stop_p; p++) {
+    const int k = w->depk[p];
+    if (k < 0) continue;
+    const Rec& r = w->rec[w->srt[p].idx];
+    if (r.prio != EV_TOOL) continue;
+    const int cur = r.inst;
+    long long bu = 0;
+    int bi = 0;
+    for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+      long long u = w->snap[k][i - 1];
+      if (!sc.include_idle && !(u > 0 || i == cur)) continue;
+      if (!bi || u < bu) {
+        bu = u;
+        bi = i;
+      }
+    }
+    for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
+      long long ou = t_shfl_xor_ll(bu, o);
+      int oi = t_shfl_xor_i(bi, o);
+      if (oi && (!bi || ou < bu || (ou == bu && oi < bi))) {
+        bu = ou;
+        bi = oi;
+      }
+    }
+    if (bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu) {
+      stop_p = p;
+      stop_kind = STOP_COUPLING;
+      break;
+    }
+  }
+  /* ---- step 3: commit per instance (usage, running, power, running log) */
+  long long turns = 0, completed = 0, events = 0;
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    Inst& in = w->in[i - 1];
+    for (int p = 0; p < stop_p; p++) {
+      Rec& r = w->rec[w->srt[p].idx];
+      if (r.inst != i) continue;
+      if (r.prio == EV_COMPLETE) {
+        in.usage += r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
+        in.running -= 1;
+        turns++;
+        events++;
+        if (r.flags & F_LAST) completed++;
+      } else {
+        in.running += 1;
+        r.logpos = in.log_len;
+        g.log[(long long)(i - 1) * g.A + in.log_len] = r.agent;
+        in.log_len++;
+        events++;
+      }
+      update_power(w, i, r.t);
+    }
+  }
+  turns = t_sum_ll(turns);
+  completed = t_sum_ll(completed);
+  events = t_sum_ll(events);
+  t_sync();
+  /* ---- step 4: push sequence numbers and start ranks (prefix scans in walk order) */
+  const long long seq0 = w->seq, rank0 = w->start_ctr;
+  int pushes = 0, starts = 0;
+  for (int base = 0; base < stop_p; base += EC_TSIZE) {
+    const int p = base + EC_LANE;
+    bool push = false, start = false;
+    Rec* r = nullptr;
+    if (p < stop_p) {
+      r = &w->rec[w->srt[p].idx];
+      start = r->prio == EV_TOOL || r->prio == EV_ISSUE;
+      push = start || (r->prio == EV_COMPLETE && !(r->flags & F_LAST));
+    }
+    unsigned mp = t_ballot(push), ms = t_ballot(start);
+    if (r) {
+      if (push) {
+        r->push_seq = seq0 + pushes + ec_popc(mp & t_lt_mask());
+        if (r->child >= 0) w->rec[r->child].seq = r->push_seq;
+      }
+      if (start) r->aux64 = rank0 + starts + ec_popc(ms & t_lt_mask());
+      r->flags |= F_COMMITTED;
+    }
+    pushes += ec_popc(mp);
+    starts += ec_popc(ms);
+  }
+  t_sync();
+  /* ---- step 5: arrivals in order (routing on the usage snapshot) */
+  for (int p = 0; p < stop_p; p++) {
+    const int k = w->depk[p];
+    if (k < 0) continue;
+    const Rec& r = w->rec[w->srt[p].idx];
+    if (r.prio != EV_ARRIVAL) continue;
+    int target;
+    if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
+      target = (w->rr_next % M) + 1;
+    } else {
+      long long bu = 0;
+      int bi = 0, light = 0x7fffffff;
+      const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+      for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+        long long u = w->snap[k][i - 1];
+        if (sc.policy == ASB_POLICY_CONTEXT_AWARE && (double)u < threshold && i < light) light = i;
+        if (!bi || u < bu) {
+          bu = u;
+          bi = i;
+        }
+      }
+      for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
+        long long ou = t_shfl_xor_ll(bu, o);
+        int oi = t_shfl_xor_i(bi, o);
+        int ol = t_shfl_xor_i(light, o);
+        light = ol < light ? ol : light;
+        if (oi && (!bi || ou < bu || (ou == bu && oi < bi))) {
+          bu = ou;
+          bi = oi;
+        }
+      }
+      target = light != 0x7fffffff ? light : bi;
+    }
+    if (EC_LANE == 0) {
+      const int a = r.agent;
+      Inst& dst = w->in[target - 1];
+      if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
+      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
+      dst.fifo_len++;
+      g.inst[a] = target;
+      g.sa[a] = 0;
+      g.phase[a] = ASB_PHASE_PENDING;
+      g.tp[a] = EC_INF;
+      g.rank[a] = w->arr_rank++;
+      g.alive[w->n_alive++] = a;
+      w->arr_ptr = (int)r.seq + 1;
+      w->ctr[ASB_CTR_ARRIVED]++;
+    }
+    t_sync();
+  }
+  if (EC_LANE == 0) {
+    w->seq += pushes;
+    w->start_ctr += starts;
+    w->ctr[ASB_CTR_TURNS] += turns;
+    w->ctr[ASB_CTR_COMPLETED] += completed;
+    w->ctr[ASB_CTR_EVENTS] += events;
+    int stop = stop_kind;
+    if (stop == STOP_NONE && (cut < n || w->hz_t != EC_INF_BITS)) stop = STOP_HORIZON;
+    const int stop_idx = (stop == STOP_COUPLING || stop == STOP_LOGFULL) ? (int)w->srt[stop_p].idx : -1;
+    w->stop_kind = stop;
+    w->stop_rec = stop_idx;
+    if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
+  }
+  t_sync();
+  return true;
+}
+
+
 /* one optimistic batch inside the current window (team) */
 template <class W, int RCAP, int DCAP, int ACAP>
 EC_DEV int batch(W* w, const GP& g, double win_end) {
   /* ---- 1. due collection (shrink the window if too many agents are due) */
+  EC_PROF_START(w);
   double bound = win_end;
   int incl = w->incl;
-  int nd = count_due(w, g, bound, incl);
+  int nd = collect_due<W, DCAP>(w, g, bound, incl);
+  const bool collected = nd <= DCAP;
   if (nd > DCAP) {
     /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
     double lo = w->now, hi = bound;
@@ -820,30 +1289,15 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     bound = lo;
     incl = 0;
   }
+  if (!collected) nd = collect_due<W, DCAP>(w, g, bound, incl);
   if (EC_LANE == 0) {
-    w->n_due = 0;
+    w->n_due = nd;
     w->hz_t = EC_INF_BITS;
     w->hz_p = 0;
     w->hz_s = 0;
   }
   t_sync();
-  for (int base = 0; base < w->n_alive; base += EC_TSIZE) {
-    int j = base + EC_LANE;
-    bool due = false;
-    int a = -1;
-    if (j < w->n_alive) {
-      a = g.alive[j];
-      if (g.next_prio[a] > 0) {
-        double t = g.next_t[a];
-        due = incl ? t <= bound : t < bound;
-      }
-    }
-    unsigned m = t_ballot(due);
-    if (due) w->due[w->n_due + ec_popc(m & t_lt_mask())] = a;
-    t_sync();
-    if (EC_LANE == 0) w->n_due += ec_popc(m);
-    t_sync();
-  }
+  EC_PROF(w, 2);
   /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
   if (EC_LANE == 0) {
     int n_arr = 0;
@@ -967,109 +1421,11 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
       t_sync();
     }
   }
-  /* ---- 5. commit walk (lane 0) */
-  if (EC_LANE == 0) {
-    const AsbScenario& sc = w->sc;
-    int stop = STOP_NONE, stop_idx = -1;
-    int p = 0;
-    while (p < n && stop == STOP_NONE) {
-      const unsigned long long tb = w->srt[p].tb;
-      const unsigned pr = w->srt[p].prio;
-      if (!key_less(tb, pr, w->hz_t, (unsigned)w->hz_p) &&
-          !(tb == w->hz_t && pr == (unsigned)w->hz_p)) {
-        stop = STOP_HORIZON;
-        break;
-      }
-      int q = p + 1;
-      while (q < n && w->srt[q].tb == tb && w->srt[q].prio == pr) q++;
-      if (q - p > 1) {
-        /* tie group: order by push sequence (every parent is already walked) */
-        for (int x = p + 1; x < q; x++) {
-          SortE e = w->srt[x];
-          long long sq = w->rec[e.idx].seq;
-          int y = x - 1;
-          while (y >= p && w->rec[w->srt[y].idx].seq > sq) {
-            w->srt[y + 1] = w->srt[y];
-            y--;
-          }
-          w->srt[y + 1] = e;
-        }
-      }
-      for (int x = p; x < q; x++) {
-        const int ri = (int)w->srt[x].idx;
-        Rec& r = w->rec[ri];
-        if (!below_horizon(tb, pr, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
-          stop = STOP_HORIZON;
-          break;
-        }
-        const double t = r.t;
-        if (r.prio == EV_COMPLETE) {
-          Inst& in = w->in[r.inst - 1];
-          long long nu = in.usage + r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
-          int flip = (nu > sc.capacity ? 1 : 0) != in.thr;
-          if (flip || sc.interference > 0) {
-            stop = STOP_COUPLING;
-            stop_idx = ri;
-            break;
-          }
-          in.running -= 1;
-          in.usage = nu;
-          w->ctr[ASB_CTR_TURNS]++;
-          w->ctr[ASB_CTR_EVENTS]++;
-          if (r.flags & F_LAST) {
-            w->ctr[ASB_CTR_COMPLETED]++;
-          } else {
-            r.push_seq = w->seq++;
-            if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
-          }
-          update_power(w, r.inst, t);
-        } else if (r.prio == EV_ARRIVAL) {
-          /* _on_arrival, engine.py:490-507 */
-          int a = r.agent;
-          int target = route_arrival(w);
-          Inst& dst = w->in[target - 1];
-          g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
-          dst.fifo_len++;
-          g.inst[a] = target;
-          g.sa[a] = 0;
-          g.phase[a] = ASB_PHASE_PENDING;
-          g.tp[a] = EC_INF;
-          g.rank[a] = w->arr_rank++;
-          g.alive[w->n_alive++] = a;
-          w->arr_ptr = (int)r.seq + 1;
-          w->ctr[ASB_CTR_ARRIVED]++;
-        } else {
-          /* EV_TOOL (maybe a reassignment check) or EV_ISSUE, then _start_turn */
-          if (((r.flags & F_CHECK) && reassign_target(w, r.inst)) || sc.interference > 0) {
-            stop = STOP_COUPLING;
-            stop_idx = ri;
-            break;
-          }
-          Inst& in = w->in[r.inst - 1];
-          if (in.log_len >= g.A) {
-            stop = STOP_LOGFULL;
-            stop_idx = ri;
-            break;
-          }
-          in.running += 1;
-          r.push_seq = w->seq++;
-          if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
-          r.aux64 = w->start_ctr++;
-          r.logpos = log_append(w, g, r.inst, r.agent);
-          w->ctr[ASB_CTR_EVENTS]++;
-          update_power(w, r.inst, t);
-        }
-        r.flags |= F_COMMITTED;
-      }
-      p = q;
-    }
-    /* something was dropped (buffer overflow): the window is not exhausted */
-    if (stop == STOP_NONE && w->hz_t != EC_INF_BITS) stop = STOP_HORIZON;
-    w->stop_kind = stop;
-    w->stop_rec = stop_idx;
-    if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
-  }
+  EC_PROF(w, 3);
+  /* ---- 5. commit walk: parallel segmented scans, serial fallback */
+  if (!walk_parallel<W, RCAP>(w, g, n)) walk_serial(w, g, n);
   t_sync();
+  EC_PROF(w, 4);
   /* ---- 6. apply committed chain prefixes (lane per agent) */
   for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
@@ -1124,8 +1480,10 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   if (stop == STOP_COUPLING) {
     Rec r = w->stop_r;
     exec_serial(w, g, r);
+    EC_PROF(w, 5);
     return BATCH_MORE;
   }
+  EC_PROF(w, 5);
   if (stop == STOP_LOGFULL) {
     log_pass(w, g, w->stop_r.inst, 0);
     return BATCH_MORE;
@@ -1265,6 +1623,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     w->start_ctr = 0;
     for (int c = 0; c < ASB_NCOUNTERS; c++) w->ctr[c] = 0;
     w->n_alive = w->rr_next = w->arr_ptr = w->arr_rank = w->status = 0;
+    for (int c = 0; c < 6; c++) w->prof[c] = 0;
   }
   t_sync();
   const long long K = sc.n_epochs;
@@ -1307,6 +1666,9 @@ EC_DEV void run_scenario(W* w, const GP& g) {
   t_sync();
   if (EC_LANE == 0) {
     w->ctr[ASB_CTR_STATUS] = w->status;
+#ifdef ASB_PROFILE
+    for (int c = 0; c < 6; c++) w->ctr[10 + c] = w->prof[c];
+#endif
     for (int c = 0; c < ASB_NCOUNTERS; c++) g.o_ctr[c] = w->ctr[c];
   }
   t_sync();

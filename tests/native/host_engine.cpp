@@ -36,6 +36,7 @@ static inline bool ec_isnan(double x) { return x != x; }
 static inline double ec_floor(double x) { return floor(x); }
 static inline unsigned long long ec_bits(double x) { unsigned long long b; memcpy(&b, &x, 8); return b; }
 static inline double ec_from_bits(unsigned long long b) { double x; memcpy(&x, &b, 8); return x; }
+static inline long long ec_clock() { return 0; }
 
 #include "../../paper_2604_16682_b200/csrc/engine_core.h"
 

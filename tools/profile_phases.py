@@ -1,0 +1,55 @@
+"""Per-phase cycle breakdown of the engine (ASB_PROFILE build) on a C5 shard.
+
+    python tools/profile_phases.py [seeds] [out.json]
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2604_16682_b200 import _build  # noqa: E402
+
+os.environ["ASB_LIB"] = _build.build_cuda(profile=True)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_16682_b200 import _abi  # noqa: E402
+from paper_2604_16682_b200.engine import DeviceBatch  # noqa: E402
+
+PHASES = ("tick_sweep", "epoch_instances", "due_collect", "arrivals+speculate+sort", "walk", "apply+serial")
+
+
+def main():
+    seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+    batch, _ = bench.build_shard(0, seeds)
+    db = DeviceBatch(batch, device="cuda:0")
+    db.run()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    db.run()
+    e1.record()
+    torch.cuda.synchronize()
+    ctr = db.outputs["counters"].cpu().numpy().reshape(-1, _abi.ASB_NCOUNTERS)
+    prof = ctr[:, 10:16].astype(np.float64)
+    tot = prof.sum(axis=1)
+    res = {
+        "scenarios": int(batch.n), "step_ms": e0.elapsed_time(e1),
+        "mean_cycles_per_scenario": float(tot.mean()), "max_cycles_per_scenario": float(tot.max()),
+        "phase_share": {p: float(prof[:, i].sum() / tot.sum()) for i, p in enumerate(PHASES)},
+        "phase_cycles_per_epoch": {p: float(prof[:, i].mean() / 3600) for i, p in enumerate(PHASES)},
+        "batches_per_scenario": float(ctr[:, _abi.CTR["batches"]].mean()),
+        "events_per_scenario": float(ctr[:, _abi.CTR["events"]].mean()),
+        "ticks_per_scenario": float(ctr[:, _abi.CTR["ticks"]].mean()),
+    }
+    print(json.dumps(res, indent=1))
+    if len(sys.argv) > 2:
+        with open(sys.argv[2], "w") as fh:
+            json.dump(res, fh, indent=1)
+
+
+if __name__ == "__main__":
+    main()
