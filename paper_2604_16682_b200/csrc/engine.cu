@@ -62,9 +62,9 @@ EC_DEV long long ec_clock() { return clock64(); }
 namespace {
 
 struct Workspace {
-  double *tp, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
+  double *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue, *s_tp, *s_next;
   long long *next_seq, *start_rank;
-  int *next_prio, *sa, *logpos, *alive;
+  int *next_prio, *sa, *logpos, *slot, *alive, *s_meta;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -83,7 +83,8 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   };
   size_t na = (size_t)(total_agents > 0 ? total_agents : 1);
   Workspace t;
-  t.tp = (double*)take(na * 8);
+  t.s_tp = (double*)take(na * 8);
+  t.s_next = (double*)take(na * 8);
   t.issue = (double*)take(na * 8);
   t.anchor = (double*)take(na * 8);
   t.rem = (double*)take(na * 8);
@@ -96,7 +97,9 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   t.next_prio = (int*)take(na * 4);
   t.sa = (int*)take(na * 4);
   t.logpos = (int*)take(na * 4);
+  t.slot = (int*)take(na * 4);
   t.alive = (int*)take(na * 4);
+  t.s_meta = (int*)take(na * 4);
   t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.ring_off = (long long*)take((size_t)(n_scen + 1) * 8);
@@ -181,7 +184,6 @@ __global__ void __launch_bounds__(WPB * 32)
     g.turn_base = tp.trace_turn_off[sc.trace_id];
     g.ctime = out.completion_time + oa;
     g.llm = out.llm_time + oa;
-    g.tp = ws.tp + oa;
     g.issue = ws.issue + oa;
     g.anchor = ws.anchor + oa;
     g.rem = ws.rem + oa;
@@ -202,7 +204,11 @@ __global__ void __launch_bounds__(WPB * 32)
     g.next_prio = ws.next_prio + oa;
     g.sa = ws.sa + oa;
     g.logpos = ws.logpos + oa;
+    g.slot = ws.slot + oa;
     g.alive = ws.alive + oa;
+    g.s_tp = ws.s_tp + oa;
+    g.s_next = ws.s_next + oa;
+    g.s_meta = ws.s_meta + oa;
     g.ring = ws.ring + ws.ring_off[s];
     g.log = ws.log + ws.ring_off[s];
     g.turn_issue = out.turn_issue ? out.turn_issue + out.turn_off[s] : nullptr;

@@ -9,22 +9,25 @@
  *
  *   1. epoch event (engine.py:436-488): the agent-tick sweep computes every
  *      instance's min running throughput over its ongoing ∪ pending agents
- *      (controller.py:96-103) in one pass over the alive list; level select,
- *      SLO boost, β/γ admission (a prefix scan over the pending FIFO) and the
- *      admitted turn starts run with lane-parallel helpers;
+ *      (controller.py:96-103) in one coalesced pass over the alive slots;
+ *      level select / SLO boost / power run lane-per-instance; β/γ admission
+ *      is a prefix scan over the pending FIFO; push sequence numbers of the
+ *      epoch's re-timings and admissions are an exclusive scan over
+ *      instances (the reference pushes them instance-major);
  *   2. due collection: agents whose next event falls before the next epoch;
  *   3. speculation (lane per agent): each agent's own event chain
  *      (complete → tool gap → next turn → …, engine.py:374-401, 509-568)
  *      inside the window, assuming the instance's thrash flag and level stay
  *      as they are — the only instance state an agent's timing reads;
- *   4. sort the records by (time, priority); ties are ordered by the
- *      reference's push sequence number (engine.py:300-301) during
- *      5. the commit walk (one lane): usage / running-count / power / router
- *      bookkeeping in exact reference order, stopping before the first event
- *      that couples agents (a completion that flips the thrash flag, a
- *      reassignment check that migrates, or any start/complete under
- *      interference) — that event is executed serially with the exact
- *      handler semantics, and speculation restarts after it;
+ *   4. sort the records by (time, priority); exact ties are ordered by the
+ *      reference's push sequence number (engine.py:300-301);
+ *   5. commit walk: the serial state machine decomposes by instance, so each
+ *      lane replays its instances' records (usage, running count, thrash
+ *      flag, power, running log) and the first coupling event is found by a
+ *      min-reduction — a completion that flips the thrash flag, a
+ *      reassignment check that migrates (evaluated on usage snapshots), or
+ *      any start/complete under interference.  That event is then executed
+ *      serially with the exact handler semantics and speculation restarts;
  *   6. apply (lane per agent): committed chain prefixes are written back.
  *
  * The file is compiled twice: by nvcc for sm_100a with the warp team
@@ -41,14 +44,17 @@
 #include "../../include/agentsim_b200.h"
 
 /* ---- team primitives: provided by the includer ----------------------------
- *   EC_DEV, EC_LANE, EC_TSIZE, t_sync(), t_ballot(p), t_lt_mask(),
- *   t_bcast_i(v,src), t_bcast_ll(v,src), t_scan_add_ll(v), t_sum_ll(v),
- *   t_min_ull(v), t_atomic_min_ull(p,v), t_atomic_add_i(p,v), ec_isnan(x),
- *   ec_floor(x), EC_NAN, EC_INF
+ *   EC_DEV, EC_LANE, EC_TSIZE, t_sync(), t_ballot(p), t_lt_mask(), ec_popc,
+ *   t_bcast_ll, t_scan_add_ll, t_sum_ll, t_shfl_xor_{ull,ll,i},
+ *   t_atomic_min_ull, t_atomic_add_i, ec_isnan, ec_floor, ec_bits,
+ *   ec_from_bits, ec_clock, EC_NAN, EC_INF, EC_INF_BITS
  */
 
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
+#endif
+#ifndef EC_SWEEP_UNROLL
+#define EC_SWEEP_UNROLL 8 /* independent loads in flight per lane in the slot sweeps */
 #endif
 
 namespace asb {
@@ -56,6 +62,7 @@ namespace asb {
 enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4 };
 enum { F_LAST = 1, F_CHECK = 2, F_COMMITTED = 4 };
 enum { STOP_NONE = 0, STOP_COUPLING = 1, STOP_HORIZON = 2, STOP_LOGFULL = 3 };
+enum { BATCH_DONE = 0, BATCH_MORE = 1, BATCH_SERIAL = 2 };
 
 /* one speculative event record (engine.py handler invocation) */
 struct Rec {
@@ -97,13 +104,17 @@ struct GP {
   const double* tool;
   const int* arr_order;
   long long turn_base;
-  /* agent state (SoA) */
-  double *ctime, *llm, *tp, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
+  /* agent state (SoA, by agent) */
+  double *ctime, *llm, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
   long long *dec, *maxctx, *ctx, *next_seq, *start_rank;
-  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos;
-  int* alive;
-  int* ring;  /* [M*A] pending FIFOs */
-  int* log;   /* [M*A] running logs (insertion order of inst.running) */
+  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos, *slot;
+  /* alive slots: the agent-tick / due sweeps read only these, coalesced */
+  int* alive;      /* slot -> agent */
+  double* s_tp;    /* running throughput; +inf = None; NaN = finished */
+  double* s_next;  /* next event time */
+  int* s_meta;     /* instance | next-event kind << 8 */
+  int* ring;       /* [M*A] pending FIFOs */
+  int* log;        /* [M*A] running logs (insertion order of inst.running) */
   /* outputs */
   double *turn_issue, *turn_done;
   AsbDecision* dec_rows;
@@ -124,17 +135,26 @@ struct WS {
   int hz_p;
   long long hz_s;
   int n_alive, rr_next, arr_ptr, arr_rank, status, incl;
-  int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i;
-  long long tmp_ll;
+  int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i, n_dep;
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
   unsigned long long tmin[MAXM];
+  /* epoch scratch (per instance) */
+  long long ep_uobs[MAXM], ep_seq[MAXM];
+  double ep_mintp[MAXM];
+  int ep_level[MAXM], ep_boost[MAXM], ep_nadm[MAXM], ep_head[MAXM], ep_retime[MAXM], ep_def[MAXM], ep_thr0[MAXM];
   int due[DCAP];
   Rec rec[RCAP];
   SortE srt[RCAP];
-  Rec stop_r;
-  int depk[RCAP];
+  /* sorted structure-of-arrays view of the records for the commit walk */
+  double sw_t[RCAP];
+  long long sw_du[RCAP];
+  int sw_idx[RCAP];
+  short sw_inst[RCAP];
+  unsigned char sw_prio[RCAP], sw_flags[RCAP];
+  int dep_pos[EC_DEPCAP];
   long long snap[EC_DEPCAP][MAXM];
+  Rec stop_r;
   long long prof[6];
   long long prof_t;
 };
@@ -142,17 +162,17 @@ struct WS {
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
  * accumulated by lane 0 and reported in counters[10..15] */
 #ifdef ASB_PROFILE
-#define EC_PROF_START(w) \
-  do {                   \
-    if (EC_LANE == 0) (w)->prof_t = ec_clock(); \
+#define EC_PROF_START(w)                            \
+  do {                                              \
+    if (EC_LANE == 0) (w)->prof_t = ec_clock();     \
   } while (0)
-#define EC_PROF(w, k)                                  \
-  do {                                                 \
-    if (EC_LANE == 0) {                                \
-      long long now_ = ec_clock();                     \
-      (w)->prof[k] += now_ - (w)->prof_t;              \
-      (w)->prof_t = now_;                              \
-    }                                                  \
+#define EC_PROF(w, k)                     \
+  do {                                    \
+    if (EC_LANE == 0) {                   \
+      long long now_ = ec_clock();        \
+      (w)->prof[k] += now_ - (w)->prof_t; \
+      (w)->prof_t = now_;                 \
+    }                                     \
   } while (0)
 #else
 #define EC_PROF_START(w) \
@@ -164,8 +184,42 @@ struct WS {
 #endif
 
 /* ----------------------------------------------------------------------------
- * small scalar helpers (any lane)
+ * small helpers
  * -------------------------------------------------------------------------- */
+
+EC_DEV int ring_idx(int head, int j, int A) {
+  int x = head + j; /* head < A, j < A */
+  return x >= A ? x - A : x;
+}
+
+EC_DEV bool key_less(unsigned long long ta, unsigned pa, unsigned long long tb, unsigned pb) {
+  return ta < tb || (ta == tb && pa < pb);
+}
+
+/* horizon key: records are committed only while (t, prio, seq) < (hz_t, hz_p, hz_s) */
+EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, unsigned long long ht, unsigned hp,
+                          long long hs) {
+  if (tb != ht) return tb < ht;
+  if (pr != hp) return pr < hp;
+  return seq < hs;
+}
+
+/* next-event bookkeeping: per-agent copy + the alive-slot copy the sweeps read */
+EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long long seq) {
+  g.next_t[a] = t;
+  g.next_prio[a] = prio;
+  g.next_seq[a] = seq;
+  const int j = g.slot[a];
+  g.s_next[j] = t;
+  g.s_meta[j] = inst | (prio << 8);
+}
+
+EC_DEV void clear_event(const GP& g, int a, int inst) {
+  g.next_prio[a] = 0;
+  g.s_meta[g.slot[a]] = inst;
+}
+
+EC_DEV void set_tp(const GP& g, int a, double tp) { g.s_tp[g.slot[a]] = tp; }
 
 template <class W>
 EC_DEV double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
@@ -179,7 +233,7 @@ EC_DEV double svc_time(const W* w, const GP& g, long long turn, int level, int c
 
 template <class W>
 EC_DEV void update_power(W* w, int i, double now) {
-  /* _update_power, engine.py:321-327 (lane 0) */
+  /* _update_power, engine.py:321-327 (one lane) */
   Inst& in = w->in[i - 1];
   double wt = in.running > 0 ? w->act[in.level - 1] : w->idle[in.level - 1];
   if (wt != in.watts) {
@@ -191,7 +245,7 @@ EC_DEV void update_power(W* w, int i, double now) {
 
 template <class W>
 EC_DEV void sync_thrash(W* w, int i, double now) {
-  /* _sync_thrash, engine.py:329-336 (lane 0) */
+  /* _sync_thrash, engine.py:329-336 (one lane) */
   Inst& in = w->in[i - 1];
   if (in.thr != in.thr_flag) {
     if (in.thr_flag)
@@ -199,7 +253,6 @@ EC_DEV void sync_thrash(W* w, int i, double now) {
     else
       in.thr_since = now;
     in.thr_flag = in.thr;
-    w->ctr[ASB_CTR_THRASH_FLIPS]++;
   }
 }
 
@@ -220,8 +273,7 @@ EC_DEV int argmin_usage(const W* w, int cand_mode, int current) {
   return best;
 }
 
-/* maybe_reassign decision given the counter already reached the interval
- * (router.py:110-128): returns the target or 0 */
+/* maybe_reassign decision once the counter reached the interval (router.py:110-128) */
 template <class W>
 EC_DEV int reassign_target(const W* w, int current) {
   int best = argmin_usage(w, w->sc.include_idle ? 0 : 1, current);
@@ -247,20 +299,40 @@ EC_DEV int route_arrival(W* w) {
   return argmin_usage(w, 0, 0);
 }
 
+/* _on_arrival bookkeeping after routing (engine.py:490-507), lane 0 */
+template <class W>
+EC_DEV void commit_arrival(W* w, const GP& g, int a, int target, int order_pos) {
+  Inst& dst = w->in[target - 1];
+  g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len, g.A)] = a;
+  dst.fifo_len++;
+  g.inst[a] = target;
+  g.sa[a] = 0;
+  g.phase[a] = ASB_PHASE_PENDING;
+  g.next_prio[a] = 0;
+  const int j = w->n_alive++;
+  g.alive[j] = a;
+  g.slot[a] = j;
+  g.s_tp[j] = EC_INF;
+  g.s_next[j] = 0.0;
+  g.s_meta[j] = target;
+  g.rank[a] = w->arr_rank++;
+  w->arr_ptr = order_pos + 1;
+  w->ctr[ASB_CTR_ARRIVED]++;
+}
+
 /* ----------------------------------------------------------------------------
  * running log: insertion-ordered `inst.running` (engine.py:239, 398, 517)
  * -------------------------------------------------------------------------- */
 
 /* Iterate instance i's running log in insertion order; live entries are
  * compacted to the front; if `retime`, each live turn is re-timed
- * (engine.py:355-372) with consecutive push sequence numbers. (team) */
+ * (engine.py:355-372) with push sequence numbers seq0, seq0+1, ...  Returns
+ * the number of live entries (== running turns).  (team) */
 template <class W>
-EC_DEV void log_pass(W* w, const GP& g, int i, int retime) {
+EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now) {
   Inst& in = w->in[i - 1];
   const int len = in.log_len;
   int* lg = g.log + (long long)(i - 1) * g.A;
-  const double now = w->now;
-  const long long seq0 = w->seq;
   const int level = in.level, running = in.running, thr = in.thr;
   int out = 0;
   for (int base = 0; base < len; base += EC_TSIZE) {
@@ -289,9 +361,7 @@ EC_DEV void log_pass(W* w, const GP& g, int i, int retime) {
         g.anchor[a] = now;
         g.rem[a] = rem;
         g.done[a] = done;
-        g.next_t[a] = done;
-        g.next_prio[a] = EV_COMPLETE;
-        g.next_seq[a] = seq0 + pos;
+        set_event(g, a, i, EV_COMPLETE, done, seq0 + pos);
       }
       g.logpos[a] = pos;
       lg[pos] = a;
@@ -301,15 +371,13 @@ EC_DEV void log_pass(W* w, const GP& g, int i, int retime) {
   }
   if (EC_LANE == 0) {
     in.log_len = out;
-    if (retime) {
-      w->seq += out;
-      w->ctr[ASB_CTR_RETIMES] += out;
-    }
+    if (retime) w->ctr[ASB_CTR_RETIMES] += out;
   }
   t_sync();
+  return out;
 }
 
-/* _conditions_changed, engine.py:344-372 (team) */
+/* _conditions_changed, engine.py:344-372 (team, serial context: uses w->seq) */
 template <class W>
 EC_DEV void cond_changed(W* w, const GP& g, int i) {
   if (EC_LANE == 0) {
@@ -325,10 +393,14 @@ EC_DEV void cond_changed(W* w, const GP& g, int i) {
     w->flag = changed && in.log_len > 0;
   }
   t_sync();
-  if (w->flag) log_pass(w, g, i, 1);
+  if (w->flag) {
+    int cnt = log_pass(w, g, i, 1, w->seq, w->now);
+    if (EC_LANE == 0) w->seq += cnt;
+    t_sync();
+  }
 }
 
-/* append agent a to instance i's running log (lane 0); returns position */
+/* append agent a to instance i's running log (one lane); returns position */
 template <class W>
 EC_DEV int log_append(W* w, const GP& g, int i, int a) {
   Inst& in = w->in[i - 1];
@@ -341,13 +413,20 @@ EC_DEV int log_append(W* w, const GP& g, int i, int a) {
  * serial handlers (exact reference semantics on committed state) — team
  * -------------------------------------------------------------------------- */
 
+template <class W>
+EC_DEV void count_flip(W* w, int i, double now) {
+  Inst& in = w->in[i - 1];
+  if (in.thr != in.thr_flag) w->ctr[ASB_CTR_THRASH_FLIPS]++;
+  sync_thrash(w, i, now);
+}
+
 /* _start_turn, engine.py:374-401 */
 template <class W>
 EC_DEV void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
   if (EC_LANE == 0) w->in[i - 1].running += 1;
   t_sync();
   cond_changed(w, g, i);
-  if (w->in[i - 1].log_len >= g.A) log_pass(w, g, i, 0);
+  if (w->in[i - 1].log_len >= g.A) log_pass(w, g, i, 0, 0, w->now);
   if (EC_LANE == 0) {
     Inst& in = w->in[i - 1];
     double now = w->now;
@@ -358,9 +437,7 @@ EC_DEV void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
     g.rem[a] = 1.0;
     g.done[a] = now + dur;
     g.phase[a] = ASB_PHASE_RUNNING;
-    g.next_t[a] = now + dur;
-    g.next_prio[a] = EV_COMPLETE;
-    g.next_seq[a] = w->seq++;
+    set_event(g, a, i, EV_COMPLETE, now + dur, w->seq++);
     g.start_rank[a] = w->start_ctr++;
     g.logpos[a] = log_append(w, g, i, a);
     update_power(w, i, now);
@@ -401,18 +478,16 @@ EC_DEV void complete_serial(W* w, const GP& g, int a) {
       in.usage -= ctx;
       g.phase[a] = ASB_PHASE_DONE;
       g.ctime[a] = now;
-      g.tp[a] = EC_NAN;
-      g.next_prio[a] = 0;
+      set_tp(g, a, EC_NAN);
+      clear_event(g, a, i);
       w->ctr[ASB_CTR_COMPLETED]++;
     } else {
       g.phase[a] = ASB_PHASE_TOOL;
-      g.tp[a] = (double)dec / lt;
-      g.next_t[a] = now + g.tool[turn];
-      g.next_prio[a] = EV_TOOL;
-      g.next_seq[a] = w->seq++;
+      set_tp(g, a, (double)dec / lt);
+      set_event(g, a, i, EV_TOOL, now + g.tool[turn], w->seq++);
     }
     in.thr = in.usage > w->sc.capacity;
-    sync_thrash(w, i, now);
+    count_flip(w, i, now);
   }
   t_sync();
   cond_changed(w, g, i);
@@ -435,7 +510,7 @@ EC_DEV void tool_serial(W* w, const GP& g, int a) {
       }
       g.sa[a] = sa;
     }
-    w->tmp_i = target;
+    w->flag = target;
     if (target) {
       double now = w->now;
       Inst& src = w->in[source - 1];
@@ -445,18 +520,18 @@ EC_DEV void tool_serial(W* w, const GP& g, int a) {
       /* migrate_context, router.py:154-176 */
       src.usage -= g.ctx[a];
       src.thr = src.usage > w->sc.capacity;
-      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
+      g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len, g.A)] = a;
       dst.fifo_len++;
       g.inst[a] = target;
       g.phase[a] = ASB_PHASE_PENDING;
       g.pissue[a] = now;
       g.notbefore[a] = now + w->sc.migration_delay;
-      g.next_prio[a] = 0;
-      sync_thrash(w, source, now);
+      clear_event(g, a, target);
+      count_flip(w, source, now);
     }
   }
   t_sync();
-  if (!w->tmp_i) {
+  if (!w->flag) {
     start_turn_serial(w, g, source, a, w->now);
     return;
   }
@@ -571,26 +646,12 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
 }
 
 /* ----------------------------------------------------------------------------
- * one scenario
+ * epoch event
  * -------------------------------------------------------------------------- */
 
-EC_DEV bool key_less(unsigned long long ta, unsigned pa, unsigned long long tb, unsigned pb) {
-  return ta < tb || (ta == tb && pa < pb);
-}
-
-template <class W>
-EC_DEV bool is_due(const W* w, double t) {
-  return w->incl ? (t <= w->bound) : (t < w->bound);
-}
-
-/* unroll depth of the alive-list sweeps: independent gathers in flight per lane */
-#ifndef EC_SWEEP_UNROLL
-#define EC_SWEEP_UNROLL 8
-#endif
-
-/* agent-tick sweep: per-instance count and min running throughput over the
- * alive list (ongoing ∪ pending of every instance), with lazy compaction of
- * finished agents.  controller.py:89-103, engine.py:437-454 (team) */
+/* agent-tick sweep over the alive slots: per-instance min running throughput
+ * (controller.py:89-103, engine.py:437-454) and the tick count; finished
+ * agents are compacted out lazily (team) */
 template <class W>
 EC_DEV void tick_sweep(W* w, const GP& g) {
   constexpr int U = EC_SWEEP_UNROLL;
@@ -601,29 +662,25 @@ EC_DEV void tick_sweep(W* w, const GP& g) {
   int cur_i = 0, dead = 0;
   unsigned long long cur_m = EC_INF_BITS;
   for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int a[U];
     double tp[U];
-    int ii[U];
+    int mt[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
-      a[u] = j < n ? g.alive[j] : -1;
+      tp[u] = j < n ? g.s_tp[j] : 0.0;
+      mt[u] = j < n ? g.s_meta[j] : -1;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      tp[u] = a[u] >= 0 ? g.tp[a[u]] : EC_NAN;
-      ii[u] = a[u] >= 0 ? g.inst[a[u]] : 0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      if (a[u] < 0) continue;
+      if (mt[u] < 0) continue;
       if (ec_isnan(tp[u])) {
         dead++;
         continue;
       }
-      if (ii[u] != cur_i) {
+      const int ii = mt[u] & 0xff;
+      if (ii != cur_i) {
         if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
-        cur_i = ii[u];
+        cur_i = ii;
         cur_m = EC_INF_BITS;
       }
       unsigned long long b = ec_bits(tp[u]);
@@ -635,15 +692,30 @@ EC_DEV void tick_sweep(W* w, const GP& g) {
   t_sync();
   if (EC_LANE == 0) w->ctr[ASB_CTR_TICKS] += n - dead_all;
   if (dead_all * 4 > n && dead_all > 0) {
-    /* order-free compaction of the alive list (in place: write index <= read index) */
+    /* order-free compaction of the slots (in place: write index <= read index) */
     int out = 0;
     for (int base = 0; base < n; base += EC_TSIZE) {
       int j = base + EC_LANE;
-      int a = j < n ? g.alive[j] : -1;
-      bool live = a >= 0 && !ec_isnan(g.tp[a]);
+      bool live = false;
+      int a = -1, mt = 0;
+      double tp = 0.0, nx = 0.0;
+      if (j < n) {
+        tp = g.s_tp[j];
+        live = !ec_isnan(tp);
+        a = g.alive[j];
+        nx = g.s_next[j];
+        mt = g.s_meta[j];
+      }
       unsigned m = t_ballot(live);
       t_sync();
-      if (live) g.alive[out + ec_popc(m & t_lt_mask())] = a;
+      if (live) {
+        const int o = out + ec_popc(m & t_lt_mask());
+        g.alive[o] = a;
+        g.s_tp[o] = tp;
+        g.s_next[o] = nx;
+        g.s_meta[o] = mt;
+        g.slot[a] = o;
+      }
       out += ec_popc(m);
       t_sync();
     }
@@ -663,7 +735,7 @@ EC_DEV int admission(W* w, const GP& g, int i, double gcap) {
   for (int base = 0; base < len; base += EC_TSIZE) {
     int j = base + EC_LANE;
     bool valid = j < len;
-    int a = valid ? ring[(head + j) % g.A] : -1;
+    int a = valid ? ring[ring_idx(head, j, g.A)] : -1;
     long long c = valid ? g.ctx[a] : 0;
     long long incl = t_scan_add_ll(c);
     long long excl = incl - c;
@@ -677,7 +749,7 @@ EC_DEV int admission(W* w, const GP& g, int i, double gcap) {
   t_sync();
   if (EC_LANE == 0) {
     in.usage = usage;
-    in.fifo_head = (head + n_adm) % (g.A > 0 ? g.A : 1);
+    in.fifo_head = ring_idx(head, n_adm, g.A);
     in.fifo_len = len - n_adm;
     in.thr = usage > w->sc.capacity;
   }
@@ -685,39 +757,115 @@ EC_DEV int admission(W* w, const GP& g, int i, double gcap) {
   return n_adm;
 }
 
-/* _on_epoch, engine.py:436-488 + control_epoch, controller.py:133-186 (team) */
+/* level select + SLO boost for instance i at the epoch (controller.py:81-86,147-163) */
 template <class W>
-EC_DEV void epoch_event(W* w, const GP& g, long long k) {
+EC_DEV int choose_level(const W* w, int i, int* boosted) {
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances, L = sc.n_levels;
-  EC_PROF_START(w);
-  tick_sweep(w, g);
-  EC_PROF(w, 0);
+  const int L = sc.n_levels;
+  const long long usage = w->in[i - 1].usage;
+  int level;
+  if (sc.variant == ASB_VARIANT_OFF)
+    level = L;
+  else if (sc.variant == ASB_VARIANT_FIXED)
+    level = sc.fixed_level;
+  else {
+    double ac = sc.alpha * (double)sc.capacity;
+    if ((double)usage >= ac)
+      level = L;
+    else
+      level = (int)ec_floor((double)usage / ac * (double)(L - 1)) + 1;
+  }
+  *boosted = 0;
+  const bool has_tp = w->tmin[i - 1] != EC_INF_BITS;
+  if (sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.boost_enabled && has_tp &&
+      ec_from_bits(w->tmin[i - 1]) < sc.slo_target) {
+    level = L;
+    *boosted = 1;
+  }
+  return level;
+}
+
+/* start the admitted agents' turns of instance i (engine.py:458-473), no
+ * interference: durations are independent, pushes numbered from seq0 (team) */
+template <class W>
+EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0) {
+  Inst& in = w->in[i - 1];
+  if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0, 0, w->now);
+  const long long rank0 = w->start_ctr;
+  const int log0 = in.log_len, lvl = in.level, thr = in.thr;
+  const double now = w->now;
+  int started = 0;
+  for (int base = 0; base < n_adm; base += EC_TSIZE) {
+    int j = base + EC_LANE;
+    bool valid = j < n_adm;
+    int a = valid ? g.ring[(long long)(i - 1) * g.A + ring_idx(head0, j, g.A)] : -1;
+    bool start = false;
+    double issue = 0.0;
+    if (valid) {
+      double pi = g.pissue[a];
+      issue = ec_isnan(pi) ? now : pi;
+      g.pissue[a] = EC_NAN;
+      start = !(now < g.notbefore[a]);
+    }
+    unsigned m = t_ballot(start);
+    int sidx = started + ec_popc(m & t_lt_mask());
+    if (valid) {
+      g.issue[a] = issue;
+      if (!start) {
+        g.phase[a] = ASB_PHASE_WAITING_START;
+        set_event(g, a, i, EV_ISSUE, g.notbefore[a], seq0 + j);
+      } else {
+        double dur = svc_time(w, g, g.aturn[a] + g.steps[a], lvl, 0, thr);
+        g.anchor[a] = now;
+        g.rem[a] = 1.0;
+        g.done[a] = now + dur;
+        g.phase[a] = ASB_PHASE_RUNNING;
+        set_event(g, a, i, EV_COMPLETE, now + dur, seq0 + j);
+        g.start_rank[a] = rank0 + sidx;
+        g.logpos[a] = log0 + sidx;
+        g.log[(long long)(i - 1) * g.A + log0 + sidx] = a;
+      }
+    }
+    started += ec_popc(m);
+  }
+  t_sync();
+  if (EC_LANE == 0) {
+    w->start_ctr += started;
+    in.running += started;
+    in.log_len += started;
+  }
+  t_sync();
+}
+
+template <class W>
+EC_DEV void write_decision(W* w, const GP& g, long long k, int i) {
+  if (!g.dec_rows) return;
+  const Inst& in = w->in[i - 1];
+  AsbDecision& d = g.dec_rows[k * w->sc.n_instances + (i - 1)];
+  d.time = w->now;
+  d.min_throughput = w->tmin[i - 1] != EC_INF_BITS ? ec_from_bits(w->tmin[i - 1]) : EC_NAN;
+  d.usage_observed = w->ep_uobs[i - 1];
+  d.instance_id = i;
+  d.frequency_level = w->ep_level[i - 1];
+  d.admitted_count = w->ep_nadm[i - 1];
+  d.pending_depth = in.fifo_len;
+  d.boosted = w->ep_boost[i - 1];
+  d.deferred = w->ep_def[i - 1];
+}
+
+/* exact serial epoch (interference mode: every start re-times its instance) */
+template <class W>
+EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances;
   for (int i = 1; i <= M; i++) {
     Inst& in = w->in[i - 1];
-    const long long usage_obs = in.usage;
-    const bool has_tp = w->tmin[i - 1] != EC_INF_BITS;
-    const double min_tp = has_tp ? ec_from_bits(w->tmin[i - 1]) : EC_NAN;
-    int level;
-    if (sc.variant == ASB_VARIANT_OFF)
-      level = L;
-    else if (sc.variant == ASB_VARIANT_FIXED)
-      level = sc.fixed_level;
-    else {
-      /* select_frequency_level, controller.py:81-86 */
-      double ac = sc.alpha * (double)sc.capacity;
-      if ((double)usage_obs >= ac)
-        level = L;
-      else
-        level = (int)ec_floor((double)usage_obs / ac * (double)(L - 1)) + 1;
+    if (EC_LANE == 0) {
+      int boosted;
+      w->ep_uobs[i - 1] = in.usage;
+      in.level = w->ep_level[i - 1] = choose_level(w, i, &boosted);
+      w->ep_boost[i - 1] = boosted;
     }
-    int boosted = 0;
-    if (sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.boost_enabled && has_tp && min_tp < sc.slo_target) {
-      level = L;
-      boosted = 1;
-    }
-    t_sync();
-    if (EC_LANE == 0) in.level = level;
     t_sync();
     cond_changed(w, g, i);
     if (EC_LANE == 0) update_power(w, i, w->now);
@@ -729,100 +877,142 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
     }
     const int head0 = in.fifo_head;
     const int n_adm = admission(w, g, i, gamma * (double)sc.capacity);
-    const int deferred = (double)in.usage > beta * (double)sc.capacity;
-    if (EC_LANE == 0) sync_thrash(w, i, w->now);
+    if (EC_LANE == 0) {
+      w->ep_nadm[i - 1] = n_adm;
+      w->ep_def[i - 1] = (double)in.usage > beta * (double)sc.capacity;
+      count_flip(w, i, w->now);
+    }
     t_sync();
     cond_changed(w, g, i);
-    /* start the admitted agents' turns in admission order (engine.py:458-473) */
-    if (sc.interference > 0) {
-      for (int j = 0; j < n_adm; j++) {
-        int a = g.ring[(long long)(i - 1) * g.A + (head0 + j) % g.A];
-        double issue = ec_isnan(g.pissue[a]) ? w->now : g.pissue[a];
-        t_sync();
-        if (EC_LANE == 0) g.pissue[a] = EC_NAN;
-        if (w->now < g.notbefore[a]) {
-          if (EC_LANE == 0) {
-            g.phase[a] = ASB_PHASE_WAITING_START;
-            g.issue[a] = issue;
-            g.next_t[a] = g.notbefore[a];
-            g.next_prio[a] = EV_ISSUE;
-            g.next_seq[a] = w->seq++;
-          }
-          t_sync();
-        } else {
-          start_turn_serial(w, g, i, a, issue);
-        }
-      }
-    } else if (n_adm > 0) {
-      if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0);
-      const long long seq0 = w->seq, rank0 = w->start_ctr;
-      const int log0 = in.log_len, lvl = in.level, thr = in.thr;
-      const double now = w->now;
-      int started = 0;
-      for (int base = 0; base < n_adm; base += EC_TSIZE) {
-        int j = base + EC_LANE;
-        bool valid = j < n_adm;
-        int a = valid ? g.ring[(long long)(i - 1) * g.A + (head0 + j) % g.A] : -1;
-        bool start = false;
-        double issue = 0.0;
-        if (valid) {
-          double pi = g.pissue[a];
-          issue = ec_isnan(pi) ? now : pi;
-          g.pissue[a] = EC_NAN;
-          start = !(now < g.notbefore[a]);
-        }
-        unsigned m = t_ballot(start);
-        int sidx = started + ec_popc(m & t_lt_mask());
-        if (valid) {
+    for (int j = 0; j < n_adm; j++) {
+      int a = g.ring[(long long)(i - 1) * g.A + ring_idx(head0, j, g.A)];
+      double issue = ec_isnan(g.pissue[a]) ? w->now : g.pissue[a];
+      const bool wait = w->now < g.notbefore[a];
+      t_sync();
+      if (EC_LANE == 0) g.pissue[a] = EC_NAN;
+      if (wait) {
+        if (EC_LANE == 0) {
+          g.phase[a] = ASB_PHASE_WAITING_START;
           g.issue[a] = issue;
-          g.next_seq[a] = seq0 + j;
-          if (!start) {
-            g.phase[a] = ASB_PHASE_WAITING_START;
-            g.next_t[a] = g.notbefore[a];
-            g.next_prio[a] = EV_ISSUE;
-          } else {
-            double dur = svc_time(w, g, g.aturn[a] + g.steps[a], lvl, 0, thr);
-            g.anchor[a] = now;
-            g.rem[a] = 1.0;
-            g.done[a] = now + dur;
-            g.next_t[a] = now + dur;
-            g.next_prio[a] = EV_COMPLETE;
-            g.phase[a] = ASB_PHASE_RUNNING;
-            g.start_rank[a] = rank0 + sidx;
-            g.logpos[a] = log0 + sidx;
-            g.log[(long long)(i - 1) * g.A + log0 + sidx] = a;
-          }
+          set_event(g, a, i, EV_ISSUE, g.notbefore[a], w->seq++);
         }
-        started += ec_popc(m);
+        t_sync();
+      } else {
+        start_turn_serial(w, g, i, a, issue);
       }
-      t_sync();
-      if (EC_LANE == 0) {
-        w->seq += n_adm;
-        w->start_ctr += started;
-        in.running += started;
-        in.log_len += started;
-      }
-      t_sync();
     }
     if (EC_LANE == 0) {
       update_power(w, i, w->now);
-      if (g.dec_rows) {
-        AsbDecision& d = g.dec_rows[k * M + (i - 1)];
-        d.time = w->now;
-        d.min_throughput = min_tp;
-        d.usage_observed = usage_obs;
-        d.instance_id = i;
-        d.frequency_level = level;
-        d.admitted_count = n_adm;
-        d.pending_depth = in.fifo_len;
-        d.boosted = boosted;
-        d.deferred = deferred;
-      }
+      write_decision(w, g, k, i);
     }
     t_sync();
   }
+}
+
+/* _on_epoch, engine.py:436-488 + control_epoch, controller.py:133-186 (team).
+ * Instances are independent within an epoch except for the instance-major
+ * order of their pushes, which an exclusive scan reproduces. */
+template <class W>
+EC_DEV void epoch_event(W* w, const GP& g, long long k) {
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances;
+  EC_PROF_START(w);
+  tick_sweep(w, g);
+  EC_PROF(w, 0);
+  if (sc.interference > 0) {
+    epoch_serial(w, g, k);
+    EC_PROF(w, 1);
+    return;
+  }
+  const double now = w->now;
+  /* (a) lane per instance: observe, level, boost, level-hook power */
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    Inst& in = w->in[i - 1];
+    int boosted;
+    w->ep_uobs[i - 1] = in.usage;
+    in.level = w->ep_level[i - 1] = choose_level(w, i, &boosted);
+    w->ep_boost[i - 1] = boosted;
+    w->ep_head[i - 1] = in.fifo_head;
+    w->ep_nadm[i - 1] = 0;
+    w->ep_thr0[i - 1] = in.thr;
+    update_power(w, i, now);
+  }
+  t_sync();
+  /* (b) β/γ admission where agents are pending (team, ascending instance) */
+  const bool ca = sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.thrash_avoidance;
+  const double gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
+  const double bcap = (ca ? sc.beta : 1.0) * (double)sc.capacity;
+  for (int i = 1; i <= M; i++) {
+    if (w->in[i - 1].fifo_len == 0) continue;
+    int n_adm = admission(w, g, i, gcap);
+    if (EC_LANE == 0) w->ep_nadm[i - 1] = n_adm;
+    t_sync();
+  }
+  /* (c) lane per instance: deferral, thrash sync, rate key, push counts;
+   * exclusive scan over instances -> each instance's first push seq */
+  long long seq_base = w->seq;
+  int flips = 0;
+  long long extra_retimes = 0;
+  for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
+    const int i = r0 + EC_LANE + 1;
+    long long pushes = 0;
+    bool flip = false;
+    if (i <= M) {
+      Inst& in = w->in[i - 1];
+      w->ep_def[i - 1] = (double)in.usage > bcap;
+      flip = in.thr != in.thr_flag;
+      sync_thrash(w, i, now);
+      /* the reference re-times twice: after the level hook (key (level,
+       * thr before admission)) and after admission (thrash flip).  Both at
+       * `now`: the second leaves rem unchanged, so one pass with the final
+       * key gives the same times; the re-time counter counts both. */
+      const int thr0 = w->ep_thr0[i - 1];
+      const int changed1 = !(in.key_valid && in.key_level == in.level && in.key_thr == thr0);
+      const int changed2 = in.thr != thr0;
+      in.key_valid = 1;
+      in.key_level = in.level;
+      in.key_thr = in.thr;
+      in.key_run = 0;
+      const int rt = (changed1 || changed2) && in.running > 0 ? in.running : 0;
+      w->ep_retime[i - 1] = rt;
+      extra_retimes += (changed1 && changed2) ? rt : 0;
+      pushes = rt + w->ep_nadm[i - 1];
+    }
+    flips += ec_popc(t_ballot(flip));
+    long long incl = t_scan_add_ll(pushes);
+    if (i <= M) w->ep_seq[i - 1] = seq_base + incl - pushes;
+    seq_base += t_bcast_ll(incl, EC_TSIZE - 1);
+  }
+  t_sync();
+  extra_retimes = t_sum_ll(extra_retimes);
+  if (EC_LANE == 0) {
+    w->seq = seq_base;
+    w->ctr[ASB_CTR_THRASH_FLIPS] += flips;
+    w->ctr[ASB_CTR_RETIMES] += extra_retimes;
+  }
+  /* (d) re-time in-flight turns where the rate key changed (team) */
+  for (int i = 1; i <= M; i++) {
+    if (!w->ep_retime[i - 1]) continue;
+    log_pass(w, g, i, 1, w->ep_seq[i - 1], now);
+  }
+  /* (e) start admitted turns, ascending instance (start ranks are global) */
+  for (int i = 1; i <= M; i++) {
+    const int n_adm = w->ep_nadm[i - 1];
+    if (!n_adm) continue;
+    start_admitted(w, g, i, w->ep_head[i - 1], n_adm, w->ep_seq[i - 1] + w->ep_retime[i - 1]);
+  }
+  /* (f) lane per instance: final power, decision rows */
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    update_power(w, i, now);
+    write_decision(w, g, k, i);
+  }
+  t_sync();
   EC_PROF(w, 1);
 }
+
+/* ----------------------------------------------------------------------------
+ * optimistic batch
+ * -------------------------------------------------------------------------- */
 
 /* count alive agents whose next event is due before `bound` (team) */
 template <class W>
@@ -831,21 +1021,17 @@ EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
   int c = 0;
   const int n = w->n_alive;
   for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int a[U], pr[U];
+    int mt[U];
     double t[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
-      a[u] = j < n ? g.alive[j] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      pr[u] = a[u] >= 0 ? g.next_prio[a[u]] : 0;
-      t[u] = a[u] >= 0 ? g.next_t[a[u]] : 0.0;
+      mt[u] = j < n ? g.s_meta[j] : 0;
+      t[u] = j < n ? g.s_next[j] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++)
-      if (pr[u] > 0 && (incl ? t[u] <= bound : t[u] < bound)) c++;
+      if ((mt[u] >> 8) > 0 && (incl ? t[u] <= bound : t[u] < bound)) c++;
   }
   return (int)t_sum_ll(c);
 }
@@ -858,24 +1044,20 @@ EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
   const int n = w->n_alive;
   int total = 0;
   for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int a[U], pr[U];
+    int mt[U];
     double t[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
-      a[u] = j < n ? g.alive[j] : -1;
+      mt[u] = j < n ? g.s_meta[j] : 0;
+      t[u] = j < n ? g.s_next[j] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      pr[u] = a[u] >= 0 ? g.next_prio[a[u]] : 0;
-      t[u] = a[u] >= 0 ? g.next_t[a[u]] : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      bool due = pr[u] > 0 && (incl ? t[u] <= bound : t[u] < bound);
+      bool due = (mt[u] >> 8) > 0 && (incl ? t[u] <= bound : t[u] < bound);
       unsigned m = t_ballot(due);
       int pos = total + ec_popc(m & t_lt_mask());
-      if (due && pos < DCAP) w->due[pos] = a[u];
+      if (due && pos < DCAP) w->due[pos] = g.alive[base + u * EC_TSIZE + EC_LANE];
       total += ec_popc(m);
     }
   }
@@ -883,19 +1065,9 @@ EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
   return total;
 }
 
-/* horizon key: records are committed only while (t, prio, seq) < (hz_t, hz_p, hz_s) */
-EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, unsigned long long ht,
-                          unsigned hp, long long hs) {
-  if (tb != ht) return tb < ht;
-  if (pr != hp) return pr < hp;
-  return seq < hs;
-}
-
-enum { BATCH_DONE = 0, BATCH_MORE = 1, BATCH_SERIAL = 2 };
-
 /* Serial commit walk (lane 0): the reference's handlers in (time, prio, seq)
  * order, stopping before the first coupling event.  Used for interference
- * mode and for tie groups whose push order is not resolved yet. */
+ * mode and for tie groups whose push order is only known during the walk. */
 template <class W>
 EC_DEV void walk_serial(W* w, const GP& g, const int n) {
   if (EC_LANE == 0) {
@@ -905,8 +1077,7 @@ EC_DEV void walk_serial(W* w, const GP& g, const int n) {
     while (p < n && stop == STOP_NONE) {
       const unsigned long long tb = w->srt[p].tb;
       const unsigned pr = w->srt[p].prio;
-      if (!key_less(tb, pr, w->hz_t, (unsigned)w->hz_p) &&
-          !(tb == w->hz_t && pr == (unsigned)w->hz_p)) {
+      if (!key_less(tb, pr, w->hz_t, (unsigned)w->hz_p) && !(tb == w->hz_t && pr == (unsigned)w->hz_p)) {
         stop = STOP_HORIZON;
         break;
       }
@@ -954,20 +1125,7 @@ EC_DEV void walk_serial(W* w, const GP& g, const int n) {
           }
           update_power(w, r.inst, t);
         } else if (r.prio == EV_ARRIVAL) {
-          /* _on_arrival, engine.py:490-507 */
-          int a = r.agent;
-          int target = route_arrival(w);
-          Inst& dst = w->in[target - 1];
-          g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
-          dst.fifo_len++;
-          g.inst[a] = target;
-          g.sa[a] = 0;
-          g.phase[a] = ASB_PHASE_PENDING;
-          g.tp[a] = EC_INF;
-          g.rank[a] = w->arr_rank++;
-          g.alive[w->n_alive++] = a;
-          w->arr_ptr = (int)r.seq + 1;
-          w->ctr[ASB_CTR_ARRIVED]++;
+          commit_arrival(w, g, r.agent, route_arrival(w), (int)r.seq);
         } else {
           /* EV_TOOL (maybe a reassignment check) or EV_ISSUE, then _start_turn */
           if (((r.flags & F_CHECK) && reassign_target(w, r.inst)) || sc.interference > 0) {
@@ -1002,6 +1160,55 @@ EC_DEV void walk_serial(W* w, const GP& g, const int n) {
   t_sync();
 }
 
+/* Per-instance replay of the sorted records [0, end) for instance i, in
+ * registers: usage, running count, running log, power.  Stops before the
+ * first thrash flip / log overflow (returned in *flip / *lf).  If `snap`,
+ * records the usage before every dependent record.  (one lane) */
+template <class W>
+EC_DEV int replay_instance(W* w, const GP& g, int i, int end, bool snap, int* flip, int* lf, Inst& st) {
+  const long long cap = w->sc.capacity;
+  const int thr = st.thr;
+  const double act = w->act[st.level - 1], idle = w->idle[st.level - 1];
+  int kk = 0;
+  int dp = (snap && w->n_dep > 0) ? w->dep_pos[0] : 0x7fffffff;
+  int p = 0;
+  for (; p < end; p++) {
+    if (dp == p) {
+      w->snap[kk][i - 1] = st.usage;
+      kk++;
+      dp = kk < w->n_dep ? w->dep_pos[kk] : 0x7fffffff;
+    }
+    if (w->sw_inst[p] != i) continue;
+    const int pr = w->sw_prio[p];
+    if (pr == EV_COMPLETE) {
+      long long nu = st.usage + w->sw_du[p];
+      if ((nu > cap ? 1 : 0) != thr) {
+        *flip = p;
+        break;
+      }
+      st.usage = nu;
+      st.running -= 1;
+    } else {
+      if (st.log_len >= g.A) {
+        *lf = p;
+        break;
+      }
+      Rec& r = w->rec[w->sw_idx[p]];
+      r.logpos = st.log_len;
+      g.log[(long long)(i - 1) * g.A + st.log_len] = r.agent;
+      st.log_len++;
+      st.running += 1;
+    }
+    const double wt = st.running > 0 ? act : idle;
+    if (wt != st.watts) {
+      const double t = w->sw_t[p];
+      st.energy += st.watts * (t - st.t_pow);
+      st.t_pow = t;
+      st.watts = wt;
+    }
+  }
+  return p;
+}
 
 /* Parallel commit walk (team).  The serial walk's state machine decomposes
  * by instance: usage, running count, thrash flag, power and the running log
@@ -1017,7 +1224,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   const AsbScenario& sc = w->sc;
   if (sc.interference > 0) return false;
   const int M = sc.n_instances;
-  /* ---- step 0: tie groups, horizon cut, dependent-record numbering */
+  /* ---- step 0: tie groups */
   int tie = 0, unknown = 0;
   for (int p = EC_LANE; p + 1 < n; p += EC_TSIZE) {
     const SortE& e0 = w->srt[p];
@@ -1048,6 +1255,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     }
     t_sync();
   }
+  /* ---- step 0b: sorted SoA view, horizon cut, dependent records */
   int cut = n;
   int ndep = 0;
   for (int base = 0; base < n; base += EC_TSIZE) {
@@ -1056,14 +1264,22 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     if (p < n) {
       const SortE& e = w->srt[p];
       const Rec& r = w->rec[e.idx];
+      w->sw_t[p] = r.t;
+      w->sw_idx[p] = (int)e.idx;
+      w->sw_prio[p] = (unsigned char)r.prio;
+      w->sw_flags[p] = (unsigned char)r.flags;
+      w->sw_inst[p] = (short)(r.prio == EV_ARRIVAL ? 0 : r.inst);
+      w->sw_du[p] = r.prio == EV_COMPLETE ? (long long)r.delta - ((r.flags & F_LAST) ? r.aux64 : 0) : 0;
       if (!below_horizon(e.tb, e.prio, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s) && p < cut) cut = p;
       dep = r.prio == EV_ARRIVAL || (r.prio == EV_TOOL && (r.flags & F_CHECK));
     }
     unsigned m = t_ballot(dep);
     int k = ndep + ec_popc(m & t_lt_mask());
-    if (p < n) {
-      w->depk[p] = dep ? k : -1;
-      if (dep && k == EC_DEPCAP && p < cut) cut = p; /* snapshot table full: stop before it */
+    if (dep) {
+      if (k < EC_DEPCAP)
+        w->dep_pos[k] = p;
+      else if (k == EC_DEPCAP && p < cut)
+        cut = p; /* snapshot table full: stop before it */
     }
     ndep += ec_popc(m);
   }
@@ -1071,35 +1287,22 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     int oc = t_shfl_xor_i(cut, o);
     cut = oc < cut ? oc : cut;
   }
+  if (EC_LANE == 0) w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
   t_sync();
-  /* ---- step 1: per-instance replay up to the cut: first flip / log overflow, snapshots */
-  int first = cut;
-  int first_lf = cut;
-  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
-    const Inst& in = w->in[i - 1];
-    long long u = in.usage;
-    const int thr = in.thr;
-    int lg = in.log_len;
-    for (int p = 0; p < cut; p++) {
-      const int k = w->depk[p];
-      if (k >= 0) w->snap[k][i - 1] = u;
-      const Rec& r = w->rec[w->srt[p].idx];
-      if (r.inst != i) continue;
-      if (r.prio == EV_COMPLETE) {
-        long long nu = u + r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
-        if ((nu > sc.capacity ? 1 : 0) != thr) {
-          if (p < first) first = p;
-          break;
-        }
-        u = nu;
-      } else if (r.prio != EV_ARRIVAL) {
-        if (lg >= g.A) {
-          if (p < first_lf) first_lf = p;
-          break;
-        }
-        lg++;
-      }
-    }
+  /* ---- step 1: per-instance replay up to the cut, in registers */
+  constexpr int NPL = (64 + EC_TSIZE - 1) / EC_TSIZE; /* instances per lane */
+  Inst st[NPL];
+  int endp[NPL];
+  int first = cut, first_lf = cut;
+#pragma unroll
+  for (int q = 0; q < NPL; q++) {
+    const int i = EC_LANE + 1 + q * EC_TSIZE;
+    if (i > M) break;
+    st[q] = w->in[i - 1];
+    int f = cut, l = cut;
+    endp[q] = replay_instance(w, g, i, cut, true, &f, &l, st[q]);
+    first = f < first ? f : first;
+    first_lf = l < first_lf ? l : first_lf;
   }
   for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
     int a = t_shfl_xor_i(first, o), b = t_shfl_xor_i(first_lf, o);
@@ -1110,12 +1313,12 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   /* ---- step 2: reassignment checks in order (team argmin on the snapshot) */
   int stop_p = first < first_lf ? first : first_lf;
   int stop_kind = stop_p == cut ? STOP_NONE : (first <= first_lf ? STOP_COUPLING : STOP_LOGFULL);
-  for (int p = 0; p < stop_p; p++) {
-    const int k = w->depk[p];
-    if (k < 0) continue;
-    const Rec& r = w->rec[w->srt[p].idx];
-    if (r.prio != EV_TOOL) continue;
-    const int cur = r.inst;
+  const int n_dep = w->n_dep;
+  for (int k = 0; k < n_dep; k++) {
+    const int p = w->dep_pos[k];
+    if (p >= stop_p) break;
+    if (w->sw_prio[p] != EV_TOOL) continue;
+    const int cur = w->sw_inst[p];
     long long bu = 0;
     int bi = 0;
     for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
@@ -1140,64 +1343,54 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
       break;
     }
   }
-  /* ---- step 3: commit per instance (usage, running, power, running log) */
-  long long turns = 0, completed = 0, events = 0;
-  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
-    Inst& in = w->in[i - 1];
-    for (int p = 0; p < stop_p; p++) {
-      Rec& r = w->rec[w->srt[p].idx];
-      if (r.inst != i) continue;
-      if (r.prio == EV_COMPLETE) {
-        in.usage += r.delta - ((r.flags & F_LAST) ? r.aux64 : 0);
-        in.running -= 1;
-        turns++;
-        events++;
-        if (r.flags & F_LAST) completed++;
-      } else {
-        in.running += 1;
-        r.logpos = in.log_len;
-        g.log[(long long)(i - 1) * g.A + in.log_len] = r.agent;
-        in.log_len++;
-        events++;
-      }
-      update_power(w, i, r.t);
+  /* ---- step 3: write back per-instance state (replay again if the stop
+   * lies before this lane's own replay end) */
+#pragma unroll
+  for (int q = 0; q < NPL; q++) {
+    const int i = EC_LANE + 1 + q * EC_TSIZE;
+    if (i > M) break;
+    if (endp[q] != stop_p) {
+      st[q] = w->in[i - 1];
+      int f = stop_p, l = stop_p;
+      replay_instance(w, g, i, stop_p, false, &f, &l, st[q]);
     }
+    w->in[i - 1] = st[q];
   }
-  turns = t_sum_ll(turns);
-  completed = t_sum_ll(completed);
-  events = t_sum_ll(events);
   t_sync();
-  /* ---- step 4: push sequence numbers and start ranks (prefix scans in walk order) */
+  /* ---- step 4: push sequence numbers, start ranks, counters (prefix scans) */
   const long long seq0 = w->seq, rank0 = w->start_ctr;
-  int pushes = 0, starts = 0;
+  int pushes = 0, starts = 0, turns = 0, completed = 0;
   for (int base = 0; base < stop_p; base += EC_TSIZE) {
     const int p = base + EC_LANE;
-    bool push = false, start = false;
-    Rec* r = nullptr;
+    bool push = false, start = false, comp = false, last = false;
     if (p < stop_p) {
-      r = &w->rec[w->srt[p].idx];
-      start = r->prio == EV_TOOL || r->prio == EV_ISSUE;
-      push = start || (r->prio == EV_COMPLETE && !(r->flags & F_LAST));
+      const int pr = w->sw_prio[p];
+      start = pr == EV_TOOL || pr == EV_ISSUE;
+      comp = pr == EV_COMPLETE;
+      last = comp && (w->sw_flags[p] & F_LAST);
+      push = start || (comp && !last);
     }
     unsigned mp = t_ballot(push), ms = t_ballot(start);
-    if (r) {
+    turns += ec_popc(t_ballot(comp));
+    completed += ec_popc(t_ballot(last));
+    if (p < stop_p) {
+      Rec& r = w->rec[w->sw_idx[p]];
       if (push) {
-        r->push_seq = seq0 + pushes + ec_popc(mp & t_lt_mask());
-        if (r->child >= 0) w->rec[r->child].seq = r->push_seq;
+        r.push_seq = seq0 + pushes + ec_popc(mp & t_lt_mask());
+        if (r.child >= 0) w->rec[r.child].seq = r.push_seq;
       }
-      if (start) r->aux64 = rank0 + starts + ec_popc(ms & t_lt_mask());
-      r->flags |= F_COMMITTED;
+      if (start) r.aux64 = rank0 + starts + ec_popc(ms & t_lt_mask());
+      r.flags |= F_COMMITTED;
     }
     pushes += ec_popc(mp);
     starts += ec_popc(ms);
   }
   t_sync();
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
-  for (int p = 0; p < stop_p; p++) {
-    const int k = w->depk[p];
-    if (k < 0) continue;
-    const Rec& r = w->rec[w->srt[p].idx];
-    if (r.prio != EV_ARRIVAL) continue;
+  for (int k = 0; k < n_dep; k++) {
+    const int p = w->dep_pos[k];
+    if (p >= stop_p) break;
+    if (w->sw_prio[p] != EV_ARRIVAL) continue;
     int target;
     if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
       target = (w->rr_next % M) + 1;
@@ -1226,19 +1419,9 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
       target = light != 0x7fffffff ? light : bi;
     }
     if (EC_LANE == 0) {
-      const int a = r.agent;
-      Inst& dst = w->in[target - 1];
+      const Rec& r = w->rec[w->sw_idx[p]];
       if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
-      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = a;
-      dst.fifo_len++;
-      g.inst[a] = target;
-      g.sa[a] = 0;
-      g.phase[a] = ASB_PHASE_PENDING;
-      g.tp[a] = EC_INF;
-      g.rank[a] = w->arr_rank++;
-      g.alive[w->n_alive++] = a;
-      w->arr_ptr = (int)r.seq + 1;
-      w->ctr[ASB_CTR_ARRIVED]++;
+      commit_arrival(w, g, r.agent, target, (int)r.seq);
     }
     t_sync();
   }
@@ -1247,10 +1430,10 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     w->start_ctr += starts;
     w->ctr[ASB_CTR_TURNS] += turns;
     w->ctr[ASB_CTR_COMPLETED] += completed;
-    w->ctr[ASB_CTR_EVENTS] += events;
+    w->ctr[ASB_CTR_EVENTS] += turns + starts;
     int stop = stop_kind;
     if (stop == STOP_NONE && (cut < n || w->hz_t != EC_INF_BITS)) stop = STOP_HORIZON;
-    const int stop_idx = (stop == STOP_COUPLING || stop == STOP_LOGFULL) ? (int)w->srt[stop_p].idx : -1;
+    const int stop_idx = (stop == STOP_COUPLING || stop == STOP_LOGFULL) ? w->sw_idx[stop_p] : -1;
     w->stop_kind = stop;
     w->stop_rec = stop_idx;
     if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
@@ -1258,7 +1441,6 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   t_sync();
   return true;
 }
-
 
 /* one optimistic batch inside the current window (team) */
 template <class W, int RCAP, int DCAP, int ACAP>
@@ -1268,7 +1450,6 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   double bound = win_end;
   int incl = w->incl;
   int nd = collect_due<W, DCAP>(w, g, bound, incl);
-  const bool collected = nd <= DCAP;
   if (nd > DCAP) {
     /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
     double lo = w->now, hi = bound;
@@ -1288,8 +1469,8 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     if (clo == 0) return BATCH_SERIAL; /* a same-timestamp burst larger than DCAP */
     bound = lo;
     incl = 0;
+    nd = collect_due<W, DCAP>(w, g, bound, incl);
   }
-  if (!collected) nd = collect_due<W, DCAP>(w, g, bound, incl);
   if (EC_LANE == 0) {
     w->n_due = nd;
     w->hz_t = EC_INF_BITS;
@@ -1424,7 +1605,6 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   EC_PROF(w, 3);
   /* ---- 5. commit walk: parallel segmented scans, serial fallback */
   if (!walk_parallel<W, RCAP>(w, g, n)) walk_serial(w, g, n);
-  t_sync();
   EC_PROF(w, 4);
   /* ---- 6. apply committed chain prefixes (lane per agent) */
   for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
@@ -1457,20 +1637,19 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     g.anchor[a] = c.anchor;
     g.rem[a] = c.rem;
     g.done[a] = c.done;
-    g.next_prio[a] = c.prio;
-    if (c.prio > 0) {
-      g.next_t[a] = c.t;
-      g.next_seq[a] = nseq;
-    }
+    if (c.prio > 0)
+      set_event(g, a, c.inst, c.prio, c.t, nseq);
+    else
+      clear_event(g, a, c.inst);
     if (srank >= 0) {
       g.start_rank[a] = srank;
       g.logpos[a] = lpos;
     }
     if (c.phase == ASB_PHASE_DONE) {
-      g.tp[a] = EC_NAN;
+      set_tp(g, a, EC_NAN);
       g.ctime[a] = c.t;
     } else if (c.llm > 0.0) {
-      g.tp[a] = (double)c.dec / c.llm;
+      set_tp(g, a, (double)c.dec / c.llm);
     }
   }
   t_sync();
@@ -1485,7 +1664,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   }
   EC_PROF(w, 5);
   if (stop == STOP_LOGFULL) {
-    log_pass(w, g, w->stop_r.inst, 0);
+    log_pass(w, g, w->stop_r.inst, 0, 0, w->now);
     return BATCH_MORE;
   }
   if (stop == STOP_HORIZON) return BATCH_MORE;
@@ -1502,16 +1681,15 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
  * (used only when a burst of identical timestamps exceeds the batch buffers) */
 template <class W>
 EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
-  /* min over alive agents' next events by (t, prio, seq) */
   unsigned long long bt = EC_INF_BITS;
   unsigned bp = 0xffffffffu;
   long long bs = 0x7fffffffffffffffll;
   int ba = -1;
   for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
-    int a = g.alive[j];
-    int pr = g.next_prio[a];
+    const int pr = g.s_meta[j] >> 8;
     if (pr <= 0) continue;
-    unsigned long long tb = ec_bits(g.next_t[a]);
+    const int a = g.alive[j];
+    unsigned long long tb = ec_bits(g.s_next[j]);
     long long s = g.next_seq[a];
     if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
       bt = tb;
@@ -1532,7 +1710,7 @@ EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
       ba = oa;
     }
   }
-  /* pending arrival competes at priority 4 */
+  /* the next arrival competes at priority 4 */
   int arr = -1;
   if (w->arr_ptr < g.A) {
     int a = g.arr_order[w->arr_ptr];
@@ -1545,18 +1723,7 @@ EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
   if (arr >= 0) {
     if (EC_LANE == 0) {
       w->now = t;
-      int target = route_arrival(w);
-      Inst& dst = w->in[target - 1];
-      g.ring[(long long)(target - 1) * g.A + (dst.fifo_head + dst.fifo_len) % g.A] = arr;
-      dst.fifo_len++;
-      g.inst[arr] = target;
-      g.sa[arr] = 0;
-      g.phase[arr] = ASB_PHASE_PENDING;
-      g.tp[arr] = EC_INF;
-      g.rank[arr] = w->arr_rank++;
-      g.alive[w->n_alive++] = arr;
-      w->arr_ptr++;
-      w->ctr[ASB_CTR_ARRIVED]++;
+      commit_arrival(w, g, arr, route_arrival(w), w->arr_ptr);
     }
     t_sync();
     return true;
@@ -1578,7 +1745,6 @@ EC_DEV void run_scenario(W* w, const GP& g) {
   for (int a = EC_LANE; a < A; a += EC_TSIZE) {
     g.ctime[a] = EC_NAN;
     g.llm[a] = 0.0;
-    g.tp[a] = EC_NAN;
     g.issue[a] = 0.0;
     g.anchor[a] = 0.0;
     g.rem[a] = 0.0;
@@ -1599,6 +1765,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     g.next_prio[a] = 0;
     g.sa[a] = 0;
     g.logpos[a] = -1;
+    g.slot[a] = -1;
   }
   if (g.turn_issue) {
     long long nt = g.aturn[A] - g.aturn[0];

@@ -62,9 +62,9 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     const long long oa = out->agent_off[s], oi = out->inst_off[s];
     size_t na = (size_t)(A > 0 ? A : 1);
     asb::GP g;
-    double* f64 = (double*)calloc(na * 8, 8);
+    double* f64 = (double*)calloc(na * 9, 8);
     long long* i64 = (long long*)calloc(na * 2, 8);
-    int* i32 = (int*)calloc(na * 4, 4);
+    int* i32 = (int*)calloc(na * 6, 4);
     int* rl = (int*)calloc(na * (size_t)sc.n_instances * 2, 4);
     g.arrival = tp->arrival + a0;
     g.aturn = (const long long*)tp->agent_turn_off + a0;
@@ -75,7 +75,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.turn_base = tp->trace_turn_off[sc.trace_id];
     g.ctime = out->completion_time + oa;
     g.llm = out->llm_time + oa;
-    g.tp = f64;
+    g.s_tp = f64 + 8 * na;
     g.issue = f64 + na;
     g.anchor = f64 + 2 * na;
     g.rem = f64 + 3 * na;
@@ -97,6 +97,9 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.sa = i32 + na;
     g.logpos = i32 + 2 * na;
     g.alive = i32 + 3 * na;
+    g.slot = i32 + 4 * na;
+    g.s_meta = i32 + 5 * na;
+    g.s_next = f64;
     g.ring = rl;
     g.log = rl + na * (size_t)sc.n_instances;
     g.turn_issue = out->turn_issue ? out->turn_issue + out->turn_off[s] : nullptr;
