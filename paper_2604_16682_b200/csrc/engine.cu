@@ -64,7 +64,7 @@ namespace {
 struct Workspace {
   double *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue, *s_tp, *s_next;
   long long *next_seq, *start_rank;
-  int *next_prio, *sa, *logpos, *slot, *alive, *s_meta;
+  int *next_prio, *sa, *logpos, *slot, *alive, *s_meta, *dstamp;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -100,6 +100,7 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   t.slot = (int*)take(na * 4);
   t.alive = (int*)take(na * 4);
   t.s_meta = (int*)take(na * 4);
+  t.dstamp = (int*)take(na * 4);
   t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.ring_off = (long long*)take((size_t)(n_scen + 1) * 8);
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(WPB * 32)
     g.s_tp = ws.s_tp + oa;
     g.s_next = ws.s_next + oa;
     g.s_meta = ws.s_meta + oa;
+    g.dstamp = ws.dstamp + oa;
     g.ring = ws.ring + ws.ring_off[s];
     g.log = ws.log + ws.ring_off[s];
     g.turn_issue = out.turn_issue ? out.turn_issue + out.turn_off[s] : nullptr;
@@ -276,8 +278,8 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
   if (max_instances <= 16)
-    return launch_engine<16, 256, 128, 64, 4>(d_scen, n_scen, traces, tables, out, ws, st);
-  return launch_engine<64, 256, 128, 64, 4>(d_scen, n_scen, traces, tables, out, ws, st);
+    return launch_engine<16, 256, 128, 64, 1>(d_scen, n_scen, traces, tables, out, ws, st);
+  return launch_engine<64, 256, 128, 64, 1>(d_scen, n_scen, traces, tables, out, ws, st);
 }
 
 }  // extern "C"

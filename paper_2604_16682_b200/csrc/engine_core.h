@@ -60,7 +60,7 @@
 namespace asb {
 
 enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4 };
-enum { F_LAST = 1, F_CHECK = 2, F_COMMITTED = 4 };
+enum { F_LAST = 1, F_CHECK = 2, F_COMMITTED = 4, F_EMPTY = 8 };
 enum { STOP_NONE = 0, STOP_COUPLING = 1, STOP_HORIZON = 2, STOP_LOGFULL = 3 };
 enum { BATCH_DONE = 0, BATCH_MORE = 1, BATCH_SERIAL = 2 };
 
@@ -74,6 +74,8 @@ struct Rec {
   short prio;          /* EV_* kind == tie-break priority */
   short flags;
   int delta;           /* COMPLETE: prefill+decode */
+  int dd;              /* COMPLETE: decode tokens */
+  double nt;           /* time of the event this one pushes (tool gap end / turn done) */
   int child;           /* next record of the same agent chain, -1 none */
   int logpos;          /* start: position in the instance running log */
   int inst;
@@ -107,7 +109,7 @@ struct GP {
   /* agent state (SoA, by agent) */
   double *ctime, *llm, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
   long long *dec, *maxctx, *ctx, *next_seq, *start_rank;
-  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos, *slot;
+  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos, *slot, *dstamp;
   /* alive slots: the agent-tick / due sweeps read only these, coalesced */
   int* alive;      /* slot -> agent */
   double* s_tp;    /* running throughput; +inf = None; NaN = finished */
@@ -136,9 +138,11 @@ struct WS {
   long long hz_s;
   int n_alive, rr_next, arr_ptr, arr_rank, status, incl;
   int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i, n_dep;
+  int due_ready, n_cand, cand_token, n_empty;
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
   unsigned long long tmin[MAXM];
+  unsigned long long part[MAXM][32]; /* per-lane partial minima of the tick sweep */
   /* epoch scratch (per instance) */
   long long ep_uobs[MAXM], ep_seq[MAXM];
   double ep_mintp[MAXM];
@@ -320,6 +324,26 @@ EC_DEV void commit_arrival(W* w, const GP& g, int a, int target, int order_pos) 
   w->ctr[ASB_CTR_ARRIVED]++;
 }
 
+/* add agents whose next event changed during the epoch (re-timed or just
+ * admitted) to the due candidates, once each (team; `cand` per lane) */
+template <class W, int DCAP>
+EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
+  bool add = false;
+  if (cand && a >= 0 && g.dstamp[a] != w->cand_token) {
+    const double t = g.next_t[a];
+    add = w->incl ? t <= w->bound : t < w->bound;
+  }
+  unsigned m = t_ballot(add);
+  if (add) {
+    const int pos = w->n_cand + ec_popc(m & t_lt_mask());
+    if (pos < DCAP) w->due[pos] = a;
+    g.dstamp[a] = w->cand_token;
+  }
+  t_sync();
+  if (EC_LANE == 0) w->n_cand += ec_popc(m);
+  t_sync();
+}
+
 /* ----------------------------------------------------------------------------
  * running log: insertion-ordered `inst.running` (engine.py:239, 398, 517)
  * -------------------------------------------------------------------------- */
@@ -328,8 +352,8 @@ EC_DEV void commit_arrival(W* w, const GP& g, int a, int target, int order_pos) 
  * compacted to the front; if `retime`, each live turn is re-timed
  * (engine.py:355-372) with push sequence numbers seq0, seq0+1, ...  Returns
  * the number of live entries (== running turns).  (team) */
-template <class W>
-EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now) {
+template <class W, int DCAP = 0>
+EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false) {
   Inst& in = w->in[i - 1];
   const int len = in.log_len;
   int* lg = g.log + (long long)(i - 1) * g.A;
@@ -368,6 +392,7 @@ EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double
     }
     out += ec_popc(m);
     t_sync();
+    if (DCAP > 0 && collect) add_candidates<W, DCAP>(w, g, live ? a : -1, retime && live);
   }
   if (EC_LANE == 0) {
     in.log_len = out;
@@ -610,15 +635,18 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
     c.llm += llm;
     if (c.ctx > c.maxctx) c.maxctx = c.ctx;
     r.delta = p + d;
+    r.dd = d;
     r.aux64 = c.ctx;
     if (c.steps == c.n_turns) {
       r.flags |= F_LAST;
       c.phase = ASB_PHASE_DONE;
       c.prio = 0;
+      r.nt = c.t;
     } else {
       c.phase = ASB_PHASE_TOOL;
       c.prio = EV_TOOL;
       c.t = c.t + g.tool[turn];
+      r.nt = c.t;
     }
     return true;
   }
@@ -642,7 +670,50 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
   c.phase = ASB_PHASE_RUNNING;
   c.prio = EV_COMPLETE;
   c.t = c.done;
+  r.nt = c.t;
   return c.t > t0;
+}
+
+/* Re-apply a committed record to the cursor from the record alone (no trace
+ * reads): the write-back half of cur_step. */
+template <class W>
+EC_DEV void cur_apply(const W* w, const GP& g, Cur& c, const Rec& r) {
+  if (r.prio == EV_COMPLETE) {
+    if (g.turn_issue) {
+      const long long turn = c.turn0 + c.steps;
+      g.turn_issue[turn - g.turn_base] = c.issue;
+      g.turn_done[turn - g.turn_base] = r.t;
+    }
+    const double llm = r.t - c.issue;
+    c.ctx += r.delta;
+    c.steps += 1;
+    c.dec += r.dd;
+    c.llm += llm;
+    if (c.ctx > c.maxctx) c.maxctx = c.ctx;
+    if (r.flags & F_LAST) {
+      c.phase = ASB_PHASE_DONE;
+      c.prio = 0;
+      c.t = r.t;
+    } else {
+      c.phase = ASB_PHASE_TOOL;
+      c.prio = EV_TOOL;
+      c.t = r.nt;
+    }
+    return;
+  }
+  if (r.prio == EV_TOOL) {
+    c.issue = r.t;
+    if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
+      c.sa += 1;
+      if (c.sa >= w->sc.reassign_interval && !w->sc.reset_only_on_reassign) c.sa = 0;
+    }
+  }
+  c.anchor = r.t;
+  c.rem = 1.0;
+  c.done = r.nt;
+  c.phase = ASB_PHASE_RUNNING;
+  c.prio = EV_COMPLETE;
+  c.t = r.nt;
 }
 
 /* ----------------------------------------------------------------------------
@@ -651,27 +722,42 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
 
 /* agent-tick sweep over the alive slots: per-instance min running throughput
  * (controller.py:89-103, engine.py:437-454) and the tick count; finished
- * agents are compacted out lazily (team) */
-template <class W>
-EC_DEV void tick_sweep(W* w, const GP& g) {
+ * agents are compacted out lazily.  With `collect`, agents whose next event
+ * falls before `bound` are gathered as the first batch's due candidates
+ * (stamped with `token`).  (team) */
+template <class W, int DCAP>
+EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
   constexpr int U = EC_SWEEP_UNROLL;
   const int M = w->sc.n_instances;
-  for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS;
-  t_sync();
+  for (int i = 0; i < M; i++) w->part[i][EC_LANE] = EC_INF_BITS;
   const int n = w->n_alive;
-  int cur_i = 0, dead = 0;
+  int cur_i = 0, dead = 0, total = 0;
   unsigned long long cur_m = EC_INF_BITS;
   for (int base = 0; base < n; base += EC_TSIZE * U) {
-    double tp[U];
-    int mt[U];
+    double tp[U], nx[U];
+    int mt[U], ag[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
       tp[u] = j < n ? g.s_tp[j] : 0.0;
       mt[u] = j < n ? g.s_meta[j] : -1;
+      if (collect) {
+        nx[u] = j < n ? g.s_next[j] : 0.0;
+        ag[u] = j < n ? g.alive[j] : -1;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
+      if (collect) {
+        bool due = mt[u] > 0 && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound);
+        unsigned m = t_ballot(due);
+        int pos = total + ec_popc(m & t_lt_mask());
+        if (due) {
+          if (pos < DCAP) w->due[pos] = ag[u];
+          g.dstamp[ag[u]] = token;
+        }
+        total += ec_popc(m);
+      }
       if (mt[u] < 0) continue;
       if (ec_isnan(tp[u])) {
         dead++;
@@ -679,7 +765,10 @@ EC_DEV void tick_sweep(W* w, const GP& g) {
       }
       const int ii = mt[u] & 0xff;
       if (ii != cur_i) {
-        if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
+        if (cur_i) {
+          unsigned long long& pm = w->part[cur_i - 1][EC_LANE];
+          if (cur_m < pm) pm = cur_m;
+        }
         cur_i = ii;
         cur_m = EC_INF_BITS;
       }
@@ -687,10 +776,25 @@ EC_DEV void tick_sweep(W* w, const GP& g) {
       if (b < cur_m) cur_m = b;
     }
   }
-  if (cur_i) t_atomic_min_ull(&w->tmin[cur_i - 1], cur_m);
+  if (cur_i) {
+    unsigned long long& pm = w->part[cur_i - 1][EC_LANE];
+    if (cur_m < pm) pm = cur_m;
+  }
   long long dead_all = t_sum_ll(dead);
   t_sync();
-  if (EC_LANE == 0) w->ctr[ASB_CTR_TICKS] += n - dead_all;
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) {
+    unsigned long long mn = EC_INF_BITS;
+    for (int l = 0; l < EC_TSIZE; l++) {
+      unsigned long long v = w->part[i][l];
+      mn = v < mn ? v : mn;
+    }
+    w->tmin[i] = mn;
+  }
+  if (EC_LANE == 0) {
+    w->ctr[ASB_CTR_TICKS] += n - dead_all;
+    w->n_cand = collect ? total : 0;
+    w->cand_token = token;
+  }
   if (dead_all * 4 > n && dead_all > 0) {
     /* order-free compaction of the slots (in place: write index <= read index) */
     int out = 0;
@@ -787,8 +891,8 @@ EC_DEV int choose_level(const W* w, int i, int* boosted) {
 
 /* start the admitted agents' turns of instance i (engine.py:458-473), no
  * interference: durations are independent, pushes numbered from seq0 (team) */
-template <class W>
-EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0) {
+template <class W, int DCAP>
+EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, bool collect) {
   Inst& in = w->in[i - 1];
   if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0, 0, w->now);
   const long long rank0 = w->start_ctr;
@@ -827,6 +931,7 @@ EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long 
       }
     }
     started += ec_popc(m);
+    if (collect) add_candidates<W, DCAP>(w, g, a, valid);
   }
   t_sync();
   if (EC_LANE == 0) {
@@ -912,15 +1017,18 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
 /* _on_epoch, engine.py:436-488 + control_epoch, controller.py:133-186 (team).
  * Instances are independent within an epoch except for the instance-major
  * order of their pushes, which an exclusive scan reproduces. */
-template <class W>
+template <class W, int DCAP>
 EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances;
+  const bool collect = sc.interference == 0;
   EC_PROF_START(w);
-  tick_sweep(w, g);
+  tick_sweep<W, DCAP>(w, g, collect, w->bound, w->incl, (int)(k + 1));
   EC_PROF(w, 0);
-  if (sc.interference > 0) {
+  if (!collect) {
     epoch_serial(w, g, k);
+    if (EC_LANE == 0) w->due_ready = 0;
+    t_sync();
     EC_PROF(w, 1);
     return;
   }
@@ -993,19 +1101,20 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   /* (d) re-time in-flight turns where the rate key changed (team) */
   for (int i = 1; i <= M; i++) {
     if (!w->ep_retime[i - 1]) continue;
-    log_pass(w, g, i, 1, w->ep_seq[i - 1], now);
+    log_pass<W, DCAP>(w, g, i, 1, w->ep_seq[i - 1], now, true);
   }
   /* (e) start admitted turns, ascending instance (start ranks are global) */
   for (int i = 1; i <= M; i++) {
     const int n_adm = w->ep_nadm[i - 1];
     if (!n_adm) continue;
-    start_admitted(w, g, i, w->ep_head[i - 1], n_adm, w->ep_seq[i - 1] + w->ep_retime[i - 1]);
+    start_admitted<W, DCAP>(w, g, i, w->ep_head[i - 1], n_adm, w->ep_seq[i - 1] + w->ep_retime[i - 1], true);
   }
   /* (f) lane per instance: final power, decision rows */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     update_power(w, i, now);
     write_decision(w, g, k, i);
   }
+  if (EC_LANE == 0) w->due_ready = w->n_cand <= DCAP;
   t_sync();
   EC_PROF(w, 1);
 }
@@ -1044,20 +1153,21 @@ EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
   const int n = w->n_alive;
   int total = 0;
   for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int mt[U];
+    int mt[U], ag[U];
     double t[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
       mt[u] = j < n ? g.s_meta[j] : 0;
       t[u] = j < n ? g.s_next[j] : 0.0;
+      ag[u] = j < n ? g.alive[j] : -1;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       bool due = (mt[u] >> 8) > 0 && (incl ? t[u] <= bound : t[u] < bound);
       unsigned m = t_ballot(due);
       int pos = total + ec_popc(m & t_lt_mask());
-      if (due && pos < DCAP) w->due[pos] = g.alive[base + u * EC_TSIZE + EC_LANE];
+      if (due && pos < DCAP) w->due[pos] = ag[u];
       total += ec_popc(m);
     }
   }
@@ -1449,7 +1559,14 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   EC_PROF_START(w);
   double bound = win_end;
   int incl = w->incl;
-  int nd = collect_due<W, DCAP>(w, g, bound, incl);
+  int nd;
+  if (w->due_ready) {
+    nd = w->n_cand; /* gathered by the tick sweep + epoch (may include agents no longer due) */
+    t_sync();
+    if (EC_LANE == 0) w->due_ready = 0;
+  } else {
+    nd = collect_due<W, DCAP>(w, g, bound, incl);
+  }
   if (nd > DCAP) {
     /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
     double lo = w->now, hi = bound;
@@ -1512,6 +1629,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     w->n_arr = n_arr;
     w->n_rec = w->n_due + n_arr;
     w->tmp_i = 0;
+    w->n_empty = 0;
   }
   t_sync();
   /* ---- 3. speculation: each lane runs its due agents' chains */
@@ -1525,6 +1643,15 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     cur_load(g, c, w->due[d]);
     Rec* r = &w->rec[d];
     r->seq = g.next_seq[c.a];
+    if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
+      /* a candidate whose event moved out of the window (re-timed) */
+      r->flags = F_EMPTY;
+      r->child = -1;
+      r->prio = 0;
+      r->agent = c.a;
+      t_atomic_add_i(&w->n_empty, 1);
+      continue;
+    }
     if (!cur_step(w, g, c, *r, false)) order_err = 1;
     while (c.prio > 0 && (incl ? c.t <= bound : c.t < bound)) {
       int slot = t_atomic_add_i(&w->tmp_i, 1) + nr0;
@@ -1570,12 +1697,13 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     t_sync();
   }
   /* ---- 4. sort by (time, prio) — bitonic over the next power of two */
-  const int n = w->n_rec;
+  const int n_all = w->n_rec;
+  const int n = n_all - w->n_empty; /* empty records sort last and are never walked */
   int np2 = 1;
-  while (np2 < n) np2 <<= 1;
+  while (np2 < n_all) np2 <<= 1;
   for (int j = EC_LANE; j < np2; j += EC_TSIZE) {
     SortE& e = w->srt[j];
-    if (j < n) {
+    if (j < n_all && !(w->rec[j].flags & F_EMPTY)) {
       e.tb = ec_bits(w->rec[j].t);
       e.prio = (unsigned)w->rec[j].prio;
     } else {
@@ -1612,12 +1740,11 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     Cur c;
     cur_load(g, c, w->due[d]);
     int ri = d;
-    Rec tmp;
     long long nseq = -1, srank = -1;
     int lpos = -1;
     while (ri >= 0 && (w->rec[ri].flags & F_COMMITTED)) {
       const Rec& r = w->rec[ri];
-      cur_step(w, g, c, tmp, true);
+      cur_apply(w, g, c, r);
       nseq = r.push_seq;
       if (r.prio != EV_COMPLETE) {
         srank = r.aux64;
@@ -1766,6 +1893,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     g.sa[a] = 0;
     g.logpos[a] = -1;
     g.slot[a] = -1;
+    g.dstamp[a] = 0;
   }
   if (g.turn_issue) {
     long long nt = g.aturn[A] - g.aturn[0];
@@ -1790,22 +1918,22 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     w->start_ctr = 0;
     for (int c = 0; c < ASB_NCOUNTERS; c++) w->ctr[c] = 0;
     w->n_alive = w->rr_next = w->arr_ptr = w->arr_rank = w->status = 0;
+    w->due_ready = w->n_cand = w->cand_token = w->n_empty = 0;
     for (int c = 0; c < 6; c++) w->prof[c] = 0;
   }
   t_sync();
   const long long K = sc.n_epochs;
   const double E = sc.epoch_length, T = sc.sim_duration;
   for (long long k = 0; k < K && w->status == 0; k++) {
-    if (EC_LANE == 0) w->now = (double)k * E;
-    t_sync();
-    epoch_event(w, g, k);
     const bool last = k + 1 == K;
     const double win_end = last ? T : (double)(k + 1) * E;
     if (EC_LANE == 0) {
+      w->now = (double)k * E;
       w->incl = last ? 1 : 0;
       w->bound = win_end;
     }
     t_sync();
+    epoch_event<W, DCAP>(w, g, k);
     for (;;) {
       if (w->status) break;
       int rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);

@@ -64,7 +64,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     asb::GP g;
     double* f64 = (double*)calloc(na * 9, 8);
     long long* i64 = (long long*)calloc(na * 2, 8);
-    int* i32 = (int*)calloc(na * 6, 4);
+    int* i32 = (int*)calloc(na * 7, 4);
     int* rl = (int*)calloc(na * (size_t)sc.n_instances * 2, 4);
     g.arrival = tp->arrival + a0;
     g.aturn = (const long long*)tp->agent_turn_off + a0;
@@ -99,6 +99,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.alive = i32 + 3 * na;
     g.slot = i32 + 4 * na;
     g.s_meta = i32 + 5 * na;
+    g.dstamp = i32 + 6 * na;
     g.s_next = f64;
     g.ring = rl;
     g.log = rl + na * (size_t)sc.n_instances;
