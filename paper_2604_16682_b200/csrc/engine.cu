@@ -56,6 +56,31 @@ EC_DEV double ec_floor(double x) { return floor(x); }
 EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__double_as_longlong(x); }
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 EC_DEV long long ec_clock() { return clock64(); }
+#define EC_TID ((int)threadIdx.x)
+EC_DEV void ec_fork_begin(int nt) { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); }
+EC_DEV void ec_fork_end(int nt) { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); }
+EC_DEV void ec_team_barrier() { asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory"); }
+EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
+EC_DEV unsigned long long t_warp_min_ull(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long x = __shfl_xor_sync(FULLMASK, v, o);
+    v = x < v ? x : v;
+  }
+  return v;
+}
+/* warp min of (time bits, prio) keys */
+EC_DEV void t_warp_min_key(unsigned long long& t, unsigned& p) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long xt = __shfl_xor_sync(FULLMASK, t, o);
+    unsigned xp = __shfl_xor_sync(FULLMASK, p, o);
+    if (xt < t || (xt == t && xp < p)) {
+      t = xt;
+      p = xp;
+    }
+  }
+}
 
 #include "engine_core.h"
 
@@ -142,14 +167,19 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
   }
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int WPB>
-__global__ void __launch_bounds__(WPB * 32)
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
+__global__ void __launch_bounds__(NT)
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
-  using W = asb::WS<MAXM, RCAP, DCAP, ACAP>;
+  /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
+   * helpers joining the slot sweeps, speculation, rank sort and apply */
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int warp = threadIdx.x >> 5;
-  W* w = reinterpret_cast<W*>(smem_raw + (size_t)warp * ((sizeof(W) + 15) / 16 * 16));
+  W* w = reinterpret_cast<W*>(smem_raw);
+  if (threadIdx.x >= 32) {
+    asb::helper_loop(w);
+    return;
+  }
   for (;;) {
     int s = 0;
     if (EC_LANE == 0) s = atomicAdd(ws.work, 1);
@@ -225,33 +255,36 @@ __global__ void __launch_bounds__(WPB * 32)
     g.A = A;
     g.M = sc.n_instances;
     g.L = sc.n_levels;
+    if (EC_LANE == 0) w->gp = g;
     __syncwarp();
     asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
     __syncwarp();
   }
+  if (EC_LANE == 0) w->job = asb::JOB_EXIT;
+  __syncwarp();
+  ec_fork_begin(NT);
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int WPB>
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
 int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp, const AsbTablePool& tb,
                   const AsbOutputs& out, const Workspace& ws, cudaStream_t st) {
-  using W = asb::WS<MAXM, RCAP, DCAP, ACAP>;
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
-  static_assert((RCAP & (RCAP - 1)) == 0, "RCAP must be a power of two");
-  const size_t per_warp = (sizeof(W) + 15) / 16 * 16;
-  const size_t smem = per_warp * WPB;
-  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, WPB>;
+  static_assert(NT % 32 == 0 && NT >= 32, "team = whole warps");
+  const size_t smem = (sizeof(W) + 15) / 16 * 16;
+  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return ASB_ERR_LAUNCH;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPB * 32, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess || per_sm < 1)
     return ASB_ERR_LAUNCH;
-  long long want = (n_scen + WPB - 1) / WPB;
+  long long want = n_scen;
   long long cap = (long long)sms * per_sm;
   int blocks = (int)(want < cap ? want : cap);
   if (blocks < 1) blocks = 1;
-  kern<<<blocks, WPB * 32, smem, st>>>(d_scen, n_scen, tp, tb, out, ws);
+  kern<<<blocks, NT, smem, st>>>(d_scen, n_scen, tp, tb, out, ws);
   return cudaGetLastError() == cudaSuccess ? ASB_OK : ASB_ERR_LAUNCH;
 }
 
@@ -278,8 +311,8 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
   if (max_instances <= 16)
-    return launch_engine<16, 256, 128, 64, 1>(d_scen, n_scen, traces, tables, out, ws, st);
-  return launch_engine<64, 256, 128, 64, 1>(d_scen, n_scen, traces, tables, out, ws, st);
+    return launch_engine<16, 256, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
+  return launch_engine<64, 256, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
 }
 
 }  // extern "C"

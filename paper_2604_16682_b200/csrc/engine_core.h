@@ -127,9 +127,26 @@ struct GP {
   int A, M, L;
 };
 
-template <int MAXM, int RCAP, int DCAP, int ACAP>
+enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5 };
+
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR>
 struct WS {
+  static constexpr int NT = NTHR;          /* threads of the team (main warp + helpers) */
+  static constexpr int NW = (NTHR + 31) / 32;
+  static constexpr int RC = RCAP, DC = DCAP, AC = ACAP;
   AsbScenario sc;
+  GP gp;                                   /* shared with the helper warps */
+  /* fork-join job state */
+  int job;
+  int j_tick, j_collect, j_incl, j_token;
+  double j_bound;
+  int j_dead, j_total, j_cut, j_tie_unknown, j_order_err;
+  unsigned long long j_hz_t[NW];
+  unsigned j_hz_p[NW];
+  unsigned long long kt[RCAP];
+  long long ks[RCAP];
+  unsigned char kp[RCAP];
+  unsigned char depflag[RCAP];
   double now, bound;
   long long seq, start_ctr;
   long long ctr[ASB_NCOUNTERS];
@@ -142,7 +159,8 @@ struct WS {
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
   unsigned long long tmin[MAXM];
-  unsigned long long part[MAXM][32]; /* per-lane partial minima of the tick sweep */
+  unsigned long long part[MAXM][NTHR]; /* per-thread partial minima of the tick sweep */
+  unsigned long long wpart[MAXM][(NTHR + 31) / 32];
   /* epoch scratch (per instance) */
   long long ep_uobs[MAXM], ep_seq[MAXM];
   double ep_mintp[MAXM];
@@ -720,45 +738,73 @@ EC_DEV void cur_apply(const W* w, const GP& g, Cur& c, const Rec& r) {
  * epoch event
  * -------------------------------------------------------------------------- */
 
-/* agent-tick sweep over the alive slots: per-instance min running throughput
- * (controller.py:89-103, engine.py:437-454) and the tick count; finished
- * agents are compacted out lazily.  With `collect`, agents whose next event
- * falls before `bound` are gathered as the first batch's due candidates
- * (stamped with `token`).  (team) */
-template <class W, int DCAP>
-EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
+/* ----------------------------------------------------------------------------
+ * fork-join over the team's helper warps
+ * -------------------------------------------------------------------------- */
+template <class W>
+EC_DEV void do_job(W* w, int job, int tid, int nthr);
+
+/* main warp: release the helper warps on `job`, take part as threads
+ * [0, 32), and join.  Helpers run helper_loop().  (1-lane host build: the
+ * job simply runs on the single lane.) */
+template <class W>
+EC_DEV void fork_job(W* w, int job) {
+  if (EC_LANE == 0) w->job = job;
+  t_sync();
+  ec_fork_begin(W::NT);
+  do_job(w, job, EC_TID, W::NT);
+  ec_fork_end(W::NT);
+}
+
+template <class W>
+EC_DEV void helper_loop(W* w) {
+  for (;;) {
+    ec_fork_begin(W::NT);
+    const int job = w->job;
+    if (job == JOB_EXIT) break;
+    do_job(w, job, EC_TID, W::NT);
+    ec_fork_end(W::NT);
+  }
+}
+
+/* JOB_SWEEP (thread-level, all warps): one pass over the alive slots.
+ * j_tick: per-instance min running throughput (per-thread partials, then a
+ * warp reduction into wpart) and the finished-slot count; j_collect: agents
+ * whose next event falls before j_bound become due candidates (stamped
+ * j_token). */
+template <class W>
+EC_DEV void job_sweep(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
   const int M = w->sc.n_instances;
-  for (int i = 0; i < M; i++) w->part[i][EC_LANE] = EC_INF_BITS;
+  const bool tick = w->j_tick, collect = w->j_collect;
+  const double bound = w->j_bound;
+  const int incl = w->j_incl, token = w->j_token;
+  if (tick)
+    for (int i = 0; i < M; i++) w->part[i][tid] = EC_INF_BITS;
   const int n = w->n_alive;
-  int cur_i = 0, dead = 0, total = 0;
+  int cur_i = 0, dead = 0;
   unsigned long long cur_m = EC_INF_BITS;
-  for (int base = 0; base < n; base += EC_TSIZE * U) {
+  for (int base = 0; base < n; base += nthr * U) {
     double tp[U], nx[U];
     int mt[U], ag[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      int j = base + u * EC_TSIZE + EC_LANE;
-      tp[u] = j < n ? g.s_tp[j] : 0.0;
-      mt[u] = j < n ? g.s_meta[j] : -1;
-      if (collect) {
-        nx[u] = j < n ? g.s_next[j] : 0.0;
-        ag[u] = j < n ? g.alive[j] : -1;
-      }
+      const int j = base + u * nthr + tid;
+      const bool ok = j < n;
+      mt[u] = ok ? g.s_meta[j] : -1;
+      tp[u] = ok && tick ? g.s_tp[j] : 0.0;
+      nx[u] = ok && collect ? g.s_next[j] : 0.0;
+      ag[u] = ok && collect ? g.alive[j] : -1;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      if (collect) {
-        bool due = mt[u] > 0 && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound);
-        unsigned m = t_ballot(due);
-        int pos = total + ec_popc(m & t_lt_mask());
-        if (due) {
-          if (pos < DCAP) w->due[pos] = ag[u];
-          g.dstamp[ag[u]] = token;
-        }
-        total += ec_popc(m);
-      }
       if (mt[u] < 0) continue;
+      if (collect && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound)) {
+        const int pos = t_atomic_add_i(&w->j_total, 1);
+        if (pos < W::DC) w->due[pos] = ag[u];
+        g.dstamp[ag[u]] = token;
+      }
+      if (!tick) continue;
       if (ec_isnan(tp[u])) {
         dead++;
         continue;
@@ -766,33 +812,57 @@ EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, 
       const int ii = mt[u] & 0xff;
       if (ii != cur_i) {
         if (cur_i) {
-          unsigned long long& pm = w->part[cur_i - 1][EC_LANE];
+          unsigned long long& pm = w->part[cur_i - 1][tid];
           if (cur_m < pm) pm = cur_m;
         }
         cur_i = ii;
         cur_m = EC_INF_BITS;
       }
-      unsigned long long b = ec_bits(tp[u]);
+      const unsigned long long b = ec_bits(tp[u]);
       if (b < cur_m) cur_m = b;
     }
   }
+  if (!tick) return;
   if (cur_i) {
-    unsigned long long& pm = w->part[cur_i - 1][EC_LANE];
+    unsigned long long& pm = w->part[cur_i - 1][tid];
     if (cur_m < pm) pm = cur_m;
   }
-  long long dead_all = t_sum_ll(dead);
-  t_sync();
+  if (dead) t_atomic_add_i(&w->j_dead, dead);
+  for (int i = 0; i < M; i++) {
+    const unsigned long long v = t_warp_min_ull(w->part[i][tid]);
+    if ((tid & 31) == 0) w->wpart[i][tid >> 5] = v;
+  }
+}
+
+/* agent-tick sweep (main warp): fork the slot sweep, fold the partial
+ * minima into tmin (controller.py:89-103, engine.py:437-454), count the
+ * ticks, and compact finished agents out lazily. */
+template <class W>
+EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
+  const int M = w->sc.n_instances;
+  const int n = w->n_alive;
+  if (EC_LANE == 0) {
+    w->j_tick = 1;
+    w->j_collect = collect;
+    w->j_bound = bound;
+    w->j_incl = incl;
+    w->j_token = token;
+    w->j_dead = 0;
+    w->j_total = 0;
+  }
+  fork_job(w, JOB_SWEEP);
   for (int i = EC_LANE; i < M; i += EC_TSIZE) {
     unsigned long long mn = EC_INF_BITS;
-    for (int l = 0; l < EC_TSIZE; l++) {
-      unsigned long long v = w->part[i][l];
+    for (int k = 0; k < W::NW; k++) {
+      const unsigned long long v = w->wpart[i][k];
       mn = v < mn ? v : mn;
     }
     w->tmin[i] = mn;
   }
+  const int dead_all = w->j_dead;
   if (EC_LANE == 0) {
     w->ctr[ASB_CTR_TICKS] += n - dead_all;
-    w->n_cand = collect ? total : 0;
+    w->n_cand = collect ? w->j_total : 0;
     w->cand_token = token;
   }
   if (dead_all * 4 > n && dead_all > 0) {
@@ -1023,7 +1093,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   const int M = sc.n_instances;
   const bool collect = sc.interference == 0;
   EC_PROF_START(w);
-  tick_sweep<W, DCAP>(w, g, collect, w->bound, w->incl, (int)(k + 1));
+  tick_sweep(w, g, collect, w->bound, w->incl, (int)(k + 1));
   EC_PROF(w, 0);
   if (!collect) {
     epoch_serial(w, g, k);
@@ -1145,34 +1215,20 @@ EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
   return (int)t_sum_ll(c);
 }
 
-/* one pass: collect due agents into w->due (up to DCAP); returns the total
- * due count (> DCAP means the list is incomplete) (team) */
+/* collect due agents into w->due (up to DCAP); returns the total due count
+ * (> DCAP means the list is incomplete).  (main warp; forks the sweep) */
 template <class W, int DCAP>
 EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
-  constexpr int U = EC_SWEEP_UNROLL;
-  const int n = w->n_alive;
-  int total = 0;
-  for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int mt[U], ag[U];
-    double t[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      int j = base + u * EC_TSIZE + EC_LANE;
-      mt[u] = j < n ? g.s_meta[j] : 0;
-      t[u] = j < n ? g.s_next[j] : 0.0;
-      ag[u] = j < n ? g.alive[j] : -1;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      bool due = (mt[u] >> 8) > 0 && (incl ? t[u] <= bound : t[u] < bound);
-      unsigned m = t_ballot(due);
-      int pos = total + ec_popc(m & t_lt_mask());
-      if (due && pos < DCAP) w->due[pos] = ag[u];
-      total += ec_popc(m);
-    }
+  if (EC_LANE == 0) {
+    w->j_tick = 0;
+    w->j_collect = 1;
+    w->j_bound = bound;
+    w->j_incl = incl;
+    w->j_token = w->cand_token;
+    w->j_total = 0;
   }
-  t_sync();
-  return total;
+  fork_job(w, JOB_SWEEP);
+  return w->j_total;
 }
 
 /* Serial commit walk (lane 0): the reference's handlers in (time, prio, seq)
@@ -1334,55 +1390,14 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   const AsbScenario& sc = w->sc;
   if (sc.interference > 0) return false;
   const int M = sc.n_instances;
-  /* ---- step 0: tie groups */
-  int tie = 0, unknown = 0;
-  for (int p = EC_LANE; p + 1 < n; p += EC_TSIZE) {
-    const SortE& e0 = w->srt[p];
-    const SortE& e1 = w->srt[p + 1];
-    if (e0.tb == e1.tb && e0.prio == e1.prio) {
-      tie = 1;
-      if (w->rec[e0.idx].seq < 0 || w->rec[e1.idx].seq < 0) unknown = 1;
-    }
-  }
-  if (t_sum_ll(unknown)) return false;
-  if (t_sum_ll(tie)) {
-    if (EC_LANE == 0) {
-      for (int p = 0; p < n;) {
-        int q = p + 1;
-        while (q < n && w->srt[q].tb == w->srt[p].tb && w->srt[q].prio == w->srt[p].prio) q++;
-        for (int x = p + 1; x < q; x++) {
-          SortE e = w->srt[x];
-          long long sq = w->rec[e.idx].seq;
-          int y = x - 1;
-          while (y >= p && w->rec[w->srt[y].idx].seq > sq) {
-            w->srt[y + 1] = w->srt[y];
-            y--;
-          }
-          w->srt[y + 1] = e;
-        }
-        p = q;
-      }
-    }
-    t_sync();
-  }
-  /* ---- step 0b: sorted SoA view, horizon cut, dependent records */
-  int cut = n;
+  /* ---- step 0: the rank sort already ordered exact ties by push seq; an
+   * unknown seq inside a tie needs the serial walk */
+  if (w->j_tie_unknown) return false;
+  int cut = w->j_cut < n ? w->j_cut : n;
   int ndep = 0;
   for (int base = 0; base < n; base += EC_TSIZE) {
     const int p = base + EC_LANE;
-    bool dep = false;
-    if (p < n) {
-      const SortE& e = w->srt[p];
-      const Rec& r = w->rec[e.idx];
-      w->sw_t[p] = r.t;
-      w->sw_idx[p] = (int)e.idx;
-      w->sw_prio[p] = (unsigned char)r.prio;
-      w->sw_flags[p] = (unsigned char)r.flags;
-      w->sw_inst[p] = (short)(r.prio == EV_ARRIVAL ? 0 : r.inst);
-      w->sw_du[p] = r.prio == EV_COMPLETE ? (long long)r.delta - ((r.flags & F_LAST) ? r.aux64 : 0) : 0;
-      if (!below_horizon(e.tb, e.prio, r.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s) && p < cut) cut = p;
-      dep = r.prio == EV_ARRIVAL || (r.prio == EV_TOOL && (r.flags & F_CHECK));
-    }
+    const bool dep = p < n && w->depflag[p];
     unsigned m = t_ballot(dep);
     int k = ndep + ec_popc(m & t_lt_mask());
     if (dep) {
@@ -1552,93 +1567,19 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   return true;
 }
 
-/* one optimistic batch inside the current window (team) */
-template <class W, int RCAP, int DCAP, int ACAP>
-EC_DEV int batch(W* w, const GP& g, double win_end) {
-  /* ---- 1. due collection (shrink the window if too many agents are due) */
-  EC_PROF_START(w);
-  double bound = win_end;
-  int incl = w->incl;
-  int nd;
-  if (w->due_ready) {
-    nd = w->n_cand; /* gathered by the tick sweep + epoch (may include agents no longer due) */
-    t_sync();
-    if (EC_LANE == 0) w->due_ready = 0;
-  } else {
-    nd = collect_due<W, DCAP>(w, g, bound, incl);
-  }
-  if (nd > DCAP) {
-    /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
-    double lo = w->now, hi = bound;
-    int clo = 0;
-    for (int it = 0; it < 128; it++) {
-      double mid = lo + (hi - lo) * 0.5;
-      if (!(mid > lo && mid < hi)) break;
-      int c = count_due(w, g, mid, 0);
-      if (c > DCAP) {
-        hi = mid;
-      } else {
-        lo = mid;
-        clo = c;
-        if (c * 2 >= DCAP) break;
-      }
-    }
-    if (clo == 0) return BATCH_SERIAL; /* a same-timestamp burst larger than DCAP */
-    bound = lo;
-    incl = 0;
-    nd = collect_due<W, DCAP>(w, g, bound, incl);
-  }
-  if (EC_LANE == 0) {
-    w->n_due = nd;
-    w->hz_t = EC_INF_BITS;
-    w->hz_p = 0;
-    w->hz_s = 0;
-  }
-  t_sync();
-  EC_PROF(w, 2);
-  /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
-  if (EC_LANE == 0) {
-    int n_arr = 0;
-    int p = w->arr_ptr;
-    const double T = w->sc.sim_duration;
-    while (p < g.A) {
-      int a = g.arr_order[p];
-      double t = g.arrival[a];
-      if (!(t < T)) break;
-      if (!(incl ? t <= bound : t < bound)) break;
-      if (n_arr == ACAP) {
-        unsigned long long tb = ec_bits(t);
-        if (below_horizon(tb, EV_ARRIVAL, p, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
-          w->hz_t = tb;
-          w->hz_p = EV_ARRIVAL;
-          w->hz_s = p;
-        }
-        break;
-      }
-      Rec& r = w->rec[w->n_due + n_arr];
-      r.t = t;
-      r.prio = EV_ARRIVAL;
-      r.agent = a;
-      r.seq = p; /* arrivals tie-break by trace order (engine.py:315-317) */
-      r.flags = 0;
-      r.child = -1;
-      r.inst = 0;
-      n_arr++;
-      p++;
-    }
-    w->n_arr = n_arr;
-    w->n_rec = w->n_due + n_arr;
-    w->tmp_i = 0;
-    w->n_empty = 0;
-  }
-  t_sync();
-  /* ---- 3. speculation: each lane runs its due agents' chains */
-  unsigned long long my_hz_t = EC_INF_BITS;
-  unsigned my_hz_p = 0;
-  int order_err = 0;
-  const int nd2 = w->n_due;
+/* JOB_SPEC (thread-level): each thread runs its due agents' own event
+ * chains inside the window; continuation records are allocated atomically;
+ * the smallest dropped key becomes the batch horizon. */
+template <class W>
+EC_DEV void job_spec(W* w, const GP& g, int tid, int nthr) {
+  const double bound = w->j_bound;
+  const int incl = w->j_incl;
+  const int nd = w->n_due;
   const int nr0 = w->n_rec;
-  for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
+  unsigned long long my_t = EC_INF_BITS;
+  unsigned my_p = 0;
+  int order_err = 0;
+  for (int d = tid; d < nd; d += nthr) {
     Cur c;
     cur_load(g, c, w->due[d]);
     Rec* r = &w->rec[d];
@@ -1654,14 +1595,14 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     }
     if (!cur_step(w, g, c, *r, false)) order_err = 1;
     while (c.prio > 0 && (incl ? c.t <= bound : c.t < bound)) {
-      int slot = t_atomic_add_i(&w->tmp_i, 1) + nr0;
-      if (slot >= RCAP) {
+      const int slot = t_atomic_add_i(&w->tmp_i, 1) + nr0;
+      if (slot >= W::RC) {
         /* dropped continuation: its seq is unknown, so nothing at its
          * (time, prio) may commit in this batch */
-        unsigned long long tb = ec_bits(c.t);
-        if (key_less(tb, (unsigned)c.prio, my_hz_t, my_hz_p)) {
-          my_hz_t = tb;
-          my_hz_p = (unsigned)c.prio;
+        const unsigned long long tb = ec_bits(c.t);
+        if (key_less(tb, (unsigned)c.prio, my_t, my_p)) {
+          my_t = tb;
+          my_p = (unsigned)c.prio;
         }
         break;
       }
@@ -1671,71 +1612,70 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
       if (!cur_step(w, g, c, *r, false)) order_err = 1;
     }
   }
-  {
-    unsigned long long k = my_hz_t;
-    unsigned kp = my_hz_p;
-    for (int off = EC_TSIZE / 2; off > 0; off >>= 1) {
-      unsigned long long ok = t_shfl_xor_ull(k, off);
-      unsigned okp = (unsigned)t_shfl_xor_i((int)kp, off);
-      if (key_less(ok, okp, k, kp)) {
-        k = ok;
-        kp = okp;
-      }
-    }
-    int oe = (int)t_sum_ll(order_err);
-    t_sync();
-    if (EC_LANE == 0) {
-      if (below_horizon(k, kp, -1, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
-        w->hz_t = k;
-        w->hz_p = (int)kp;
-        w->hz_s = -1;
-      }
-      int extra = w->tmp_i;
-      w->n_rec = nr0 + (extra < RCAP - nr0 ? extra : RCAP - nr0);
-      if (oe) w->status = ASB_SIMERR_ORDER;
-    }
-    t_sync();
+  if (order_err) w->j_order_err = 1;
+  t_warp_min_key(my_t, my_p);
+  if ((tid & 31) == 0) {
+    w->j_hz_t[tid >> 5] = my_t;
+    w->j_hz_p[tid >> 5] = my_p;
   }
-  /* ---- 4. sort by (time, prio) — bitonic over the next power of two */
+}
+
+/* JOB_SORT (thread-level): rank sort of the records by (time, prio, seq) —
+ * seq only breaks exact (time, prio) ties, and an unknown seq in a tie sends
+ * the walk to the serial fallback — writing the sorted SoA view, the
+ * dependent-record flags and the horizon cut. */
+template <class W>
+EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
-  const int n = n_all - w->n_empty; /* empty records sort last and are never walked */
-  int np2 = 1;
-  while (np2 < n_all) np2 <<= 1;
-  for (int j = EC_LANE; j < np2; j += EC_TSIZE) {
-    SortE& e = w->srt[j];
-    if (j < n_all && !(w->rec[j].flags & F_EMPTY)) {
-      e.tb = ec_bits(w->rec[j].t);
-      e.prio = (unsigned)w->rec[j].prio;
-    } else {
-      e.tb = ~0ull;
-      e.prio = 0xffffffffu;
-    }
-    e.idx = (unsigned)j;
+  for (int j = tid; j < n_all; j += nthr) {
+    const Rec& r = w->rec[j];
+    const bool empty = r.flags & F_EMPTY;
+    w->kt[j] = empty ? ~0ull : ec_bits(r.t);
+    w->kp[j] = empty ? 0xff : (unsigned char)r.prio;
+    w->ks[j] = r.seq;
   }
-  t_sync();
-  for (int kk = 2; kk <= np2; kk <<= 1) {
-    for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-      for (int x = EC_LANE; x < np2; x += EC_TSIZE) {
-        int y = x ^ jj;
-        if (y > x) {
-          SortE ex = w->srt[x], ey = w->srt[y];
-          bool up = (x & kk) == 0;
-          bool gt = key_less(ey.tb, ey.prio, ex.tb, ex.prio);
-          if (gt == up) {
-            w->srt[x] = ey;
-            w->srt[y] = ex;
-          }
-        }
+  ec_team_barrier();
+  int tie_unknown = 0;
+  for (int j = tid; j < n_all; j += nthr) {
+    if (w->kp[j] == 0xff) continue;
+    const unsigned long long tj = w->kt[j];
+    const unsigned pj = w->kp[j];
+    const long long sj = w->ks[j];
+    int rank = 0;
+    for (int q = 0; q < n_all; q++) {
+      const unsigned long long tq = w->kt[q];
+      const unsigned pq = w->kp[q];
+      if (tq < tj || (tq == tj && pq < pj)) {
+        rank++;
+      } else if (tq == tj && pq == pj && q != j) {
+        const long long sq = w->ks[q];
+        if (sq < 0 || sj < 0) tie_unknown = 1;
+        if (sq < sj || (sq == sj && q < j)) rank++;
       }
-      t_sync();
     }
+    const Rec& r = w->rec[j];
+    SortE& e = w->srt[rank];
+    e.tb = tj;
+    e.prio = pj;
+    e.idx = (unsigned)j;
+    w->sw_t[rank] = r.t;
+    w->sw_idx[rank] = j;
+    w->sw_prio[rank] = (unsigned char)pj;
+    w->sw_flags[rank] = (unsigned char)r.flags;
+    w->sw_inst[rank] = (short)(pj == EV_ARRIVAL ? 0 : r.inst);
+    w->sw_du[rank] = pj == EV_COMPLETE ? (long long)r.delta - ((r.flags & F_LAST) ? r.aux64 : 0) : 0;
+    w->depflag[rank] = pj == EV_ARRIVAL || (pj == EV_TOOL && (r.flags & F_CHECK));
+    if (!below_horizon(tj, pj, sj, w->hz_t, (unsigned)w->hz_p, w->hz_s)) t_atomic_min_i(&w->j_cut, rank);
   }
-  EC_PROF(w, 3);
-  /* ---- 5. commit walk: parallel segmented scans, serial fallback */
-  if (!walk_parallel<W, RCAP>(w, g, n)) walk_serial(w, g, n);
-  EC_PROF(w, 4);
-  /* ---- 6. apply committed chain prefixes (lane per agent) */
-  for (int d = EC_LANE; d < nd2; d += EC_TSIZE) {
+  if (tie_unknown) w->j_tie_unknown = 1;
+}
+
+/* JOB_APPLY (thread-level): write back every due agent's committed chain
+ * prefix (records carry everything, no trace reads) and its alive slot. */
+template <class W>
+EC_DEV void job_apply(W* w, const GP& g, int tid, int nthr) {
+  const int nd = w->n_due;
+  for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
     Cur c;
     cur_load(g, c, w->due[d]);
@@ -1779,7 +1719,179 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
       set_tp(g, a, (double)c.dec / c.llm);
     }
   }
+}
+
+/* JOB_INIT (thread-level): per-agent state of a fresh scenario (engine.py:251-276) */
+template <class W>
+EC_DEV void job_init(W* w, const GP& g, int tid, int nthr) {
+  const int A = g.A;
+  for (int a = tid; a < A; a += nthr) {
+    g.ctime[a] = EC_NAN;
+    g.llm[a] = 0.0;
+    g.issue[a] = 0.0;
+    g.anchor[a] = 0.0;
+    g.rem[a] = 0.0;
+    g.done[a] = 0.0;
+    g.next_t[a] = 0.0;
+    g.notbefore[a] = 0.0;
+    g.pissue[a] = EC_NAN;
+    g.dec[a] = 0;
+    g.maxctx[a] = 0;
+    g.ctx[a] = 0;
+    g.next_seq[a] = 0;
+    g.start_rank[a] = -1;
+    g.steps[a] = 0;
+    g.inst[a] = 0;
+    g.mig[a] = 0;
+    g.phase[a] = ASB_PHASE_ARRIVING;
+    g.rank[a] = -1;
+    g.next_prio[a] = 0;
+    g.sa[a] = 0;
+    g.logpos[a] = -1;
+    g.slot[a] = -1;
+    g.dstamp[a] = 0;
+  }
+  if (g.turn_issue) {
+    const long long nt = g.aturn[A] - g.aturn[0];
+    const long long t0 = g.aturn[0] - g.turn_base;
+    for (long long t = tid; t < nt; t += nthr) {
+      g.turn_issue[t0 + t] = EC_NAN;
+      g.turn_done[t0 + t] = EC_NAN;
+    }
+  }
+}
+
+template <class W>
+EC_DEV void do_job(W* w, int job, int tid, int nthr) {
+  const GP& g = w->gp;
+  switch (job) {
+    case JOB_INIT: job_init(w, g, tid, nthr); break;
+    case JOB_SWEEP: job_sweep(w, g, tid, nthr); break;
+    case JOB_SPEC: job_spec(w, g, tid, nthr); break;
+    case JOB_SORT: job_sort(w, g, tid, nthr); break;
+    case JOB_APPLY: job_apply(w, g, tid, nthr); break;
+    default: break;
+  }
+}
+
+/* one optimistic batch inside the current window (main warp, forks jobs) */
+template <class W, int RCAP, int DCAP, int ACAP>
+EC_DEV int batch(W* w, const GP& g, double win_end) {
+  /* ---- 1. due collection (shrink the window if too many agents are due) */
+  EC_PROF_START(w);
+  double bound = win_end;
+  int incl = w->incl;
+  int nd;
+  if (w->due_ready) {
+    nd = w->n_cand; /* gathered by the tick sweep + epoch (may include agents no longer due) */
+    t_sync();
+    if (EC_LANE == 0) w->due_ready = 0;
+  } else {
+    nd = collect_due<W, DCAP>(w, g, bound, incl);
+  }
+  if (nd > DCAP) {
+    /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
+    double lo = w->now, hi = bound;
+    int clo = 0;
+    for (int it = 0; it < 128; it++) {
+      double mid = lo + (hi - lo) * 0.5;
+      if (!(mid > lo && mid < hi)) break;
+      int c = count_due(w, g, mid, 0);
+      if (c > DCAP) {
+        hi = mid;
+      } else {
+        lo = mid;
+        clo = c;
+        if (c * 2 >= DCAP) break;
+      }
+    }
+    if (clo == 0) return BATCH_SERIAL; /* a same-timestamp burst larger than DCAP */
+    bound = lo;
+    incl = 0;
+    nd = collect_due<W, DCAP>(w, g, bound, incl);
+  }
   t_sync();
+  if (EC_LANE == 0) {
+    w->n_due = nd;
+    w->hz_t = EC_INF_BITS;
+    w->hz_p = 0;
+    w->hz_s = 0;
+  }
+  t_sync();
+  EC_PROF(w, 2);
+  /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
+  if (EC_LANE == 0) {
+    int n_arr = 0;
+    int p = w->arr_ptr;
+    const double T = w->sc.sim_duration;
+    while (p < g.A) {
+      int a = g.arr_order[p];
+      double t = g.arrival[a];
+      if (!(t < T)) break;
+      if (!(incl ? t <= bound : t < bound)) break;
+      if (n_arr == ACAP) {
+        unsigned long long tb = ec_bits(t);
+        if (below_horizon(tb, EV_ARRIVAL, p, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+          w->hz_t = tb;
+          w->hz_p = EV_ARRIVAL;
+          w->hz_s = p;
+        }
+        break;
+      }
+      Rec& r = w->rec[w->n_due + n_arr];
+      r.t = t;
+      r.prio = EV_ARRIVAL;
+      r.agent = a;
+      r.seq = p; /* arrivals tie-break by trace order (engine.py:315-317) */
+      r.flags = 0;
+      r.child = -1;
+      r.inst = 0;
+      n_arr++;
+      p++;
+    }
+    w->n_arr = n_arr;
+    w->n_rec = w->n_due + n_arr;
+    w->tmp_i = 0;
+    w->n_empty = 0;
+    w->j_bound = bound;
+    w->j_incl = incl;
+    w->j_order_err = 0;
+  }
+  /* ---- 3. speculation */
+  fork_job(w, JOB_SPEC);
+  {
+    unsigned long long k = EC_INF_BITS;
+    unsigned kp = 0;
+    for (int q = 0; q < W::NW; q++)
+      if (key_less(w->j_hz_t[q], w->j_hz_p[q], k, kp)) {
+        k = w->j_hz_t[q];
+        kp = w->j_hz_p[q];
+      }
+    t_sync();
+    if (EC_LANE == 0) {
+      if (below_horizon(k, kp, -1, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
+        w->hz_t = k;
+        w->hz_p = (int)kp;
+        w->hz_s = -1;
+      }
+      const int nr0 = w->n_rec;
+      const int extra = w->tmp_i;
+      w->n_rec = nr0 + (extra < RCAP - nr0 ? extra : RCAP - nr0);
+      if (w->j_order_err) w->status = ASB_SIMERR_ORDER;
+      w->j_cut = 0x7fffffff;
+      w->j_tie_unknown = 0;
+    }
+    t_sync();
+  }
+  /* ---- 4. rank sort + sorted SoA view */
+  fork_job(w, JOB_SORT);
+  const int n = w->n_rec - w->n_empty; /* empty records rank last and are never walked */
+  EC_PROF(w, 3);
+  /* ---- 5. commit walk: parallel segmented scans, serial fallback */
+  if (!walk_parallel<W, RCAP>(w, g, n)) walk_serial(w, g, n);
+  EC_PROF(w, 4);
+  /* ---- 6. apply committed chain prefixes */
+  fork_job(w, JOB_APPLY);
   if (EC_LANE == 0) w->ctr[ASB_CTR_BATCHES]++;
   /* ---- 7. coupling / overflow follow-ups */
   const int stop = w->stop_kind;
@@ -1867,41 +1979,9 @@ EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
 template <class W, int RCAP, int DCAP, int ACAP>
 EC_DEV void run_scenario(W* w, const GP& g) {
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances, L = sc.n_levels, A = g.A;
+  const int M = sc.n_instances, L = sc.n_levels;
   /* ---- init (engine.py:251-276) */
-  for (int a = EC_LANE; a < A; a += EC_TSIZE) {
-    g.ctime[a] = EC_NAN;
-    g.llm[a] = 0.0;
-    g.issue[a] = 0.0;
-    g.anchor[a] = 0.0;
-    g.rem[a] = 0.0;
-    g.done[a] = 0.0;
-    g.next_t[a] = 0.0;
-    g.notbefore[a] = 0.0;
-    g.pissue[a] = EC_NAN;
-    g.dec[a] = 0;
-    g.maxctx[a] = 0;
-    g.ctx[a] = 0;
-    g.next_seq[a] = 0;
-    g.start_rank[a] = -1;
-    g.steps[a] = 0;
-    g.inst[a] = 0;
-    g.mig[a] = 0;
-    g.phase[a] = ASB_PHASE_ARRIVING;
-    g.rank[a] = -1;
-    g.next_prio[a] = 0;
-    g.sa[a] = 0;
-    g.logpos[a] = -1;
-    g.slot[a] = -1;
-    g.dstamp[a] = 0;
-  }
-  if (g.turn_issue) {
-    long long nt = g.aturn[A] - g.aturn[0];
-    for (long long t = EC_LANE; t < nt; t += EC_TSIZE) {
-      g.turn_issue[g.aturn[0] - g.turn_base + t] = EC_NAN;
-      g.turn_done[g.aturn[0] - g.turn_base + t] = EC_NAN;
-    }
-  }
+  fork_job(w, JOB_INIT);
   for (int i = EC_LANE; i < M; i += EC_TSIZE) {
     Inst& in = w->in[i];
     in.usage = 0;

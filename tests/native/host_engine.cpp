@@ -37,6 +37,13 @@ static inline double ec_floor(double x) { return floor(x); }
 static inline unsigned long long ec_bits(double x) { unsigned long long b; memcpy(&b, &x, 8); return b; }
 static inline double ec_from_bits(unsigned long long b) { double x; memcpy(&x, &b, 8); return x; }
 static inline long long ec_clock() { return 0; }
+#define EC_TID 0
+static inline void ec_fork_begin(int) {}
+static inline void ec_fork_end(int) {}
+static inline void ec_team_barrier() {}
+static inline int t_atomic_min_i(int* p, int v) { int o = *p; if (v < o) *p = v; return o; }
+static inline unsigned long long t_warp_min_ull(unsigned long long v) { return v; }
+static inline void t_warp_min_key(unsigned long long&, unsigned&) {}
 
 #include "../../paper_2604_16682_b200/csrc/engine_core.h"
 
@@ -44,7 +51,7 @@ static inline long long ec_clock() { return 0; }
 template <int RCAP, int DCAP, int ACAP>
 static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* tp, const AsbTablePool* tb,
                    const AsbOutputs* out) {
-  using W = asb::WS<64, RCAP, DCAP, ACAP>;
+  using W = asb::WS<64, RCAP, DCAP, ACAP, 1>;
   W* w = (W*)calloc(1, sizeof(W));
   int err = 0;
   for (int s = 0; s < n_scen; s++) {
@@ -115,6 +122,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.A = A;
     g.M = sc.n_instances;
     g.L = sc.n_levels;
+    w->gp = g;
     asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
     err |= (int)g.o_ctr[ASB_CTR_STATUS];
     free(f64);
