@@ -20,6 +20,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200.so")
 PROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_prof.so")
+WPROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_wprof.so")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "build", "liboracle.so")
 HOST_ENGINE_LIB = os.path.join(ROOT, "tests", "native", "build", "libhost_engine.so")
 
@@ -48,17 +49,19 @@ def _run(cmd: list[str]) -> None:
         raise RuntimeError(f"build failed: {' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
 
 
-def build_cuda(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str = False) -> str:
     """The product library; ``profile=True`` builds the phase-timing variant
     (-DASB_PROFILE, counters[10..15]) used only by tools/profile_phases.py."""
     srcs = [os.path.join(CSRC, f) for f in ("engine.cu", "unit_ops.cu")]
     deps = srcs + [os.path.join(CSRC, "engine_core.h"), os.path.join(ROOT, "include", "agentsim_b200.h")]
-    target = PROF_LIB_PATH if profile else LIB_PATH
+    target = WPROF_LIB_PATH if profile == "walk" else (PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
         cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", target + ".tmp", *srcs]
         if profile:
             cmd.insert(1, "-DASB_PROFILE")
+        if profile == "walk":
+            cmd.insert(1, "-DASB_PROFILE_WALK")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
@@ -91,6 +94,7 @@ def build_host_engine(force: bool = False) -> str:
 def build_all(force: bool = False) -> None:
     build_cuda(force)
     build_cuda(force, profile=True)
+    build_cuda(force, profile="walk")
     build_oracle(force)
     build_host_engine(force)
 

@@ -168,7 +168,7 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
 }
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 4)
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are

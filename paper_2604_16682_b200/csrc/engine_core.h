@@ -182,8 +182,34 @@ struct WS {
 };
 
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
- * accumulated by lane 0 and reported in counters[10..15] */
-#ifdef ASB_PROFILE
+ * accumulated by lane 0 and reported in counters[10..15];
+ * -DASB_PROFILE -DASB_PROFILE_WALK times the commit-walk steps instead */
+#if defined(ASB_PROFILE) && defined(ASB_PROFILE_WALK)
+#define EC_WPROF_START(w) \
+  do {                    \
+    if (EC_LANE == 0) (w)->prof_t = ec_clock(); \
+  } while (0)
+#define EC_WPROF(w, k)                    \
+  do {                                    \
+    if (EC_LANE == 0) {                   \
+      long long now_ = ec_clock();        \
+      (w)->prof[k] += now_ - (w)->prof_t; \
+      (w)->prof_t = now_;                 \
+    }                                     \
+  } while (0)
+#define EC_PROF_START(w) \
+  do {                   \
+  } while (0)
+#define EC_PROF(w, k) \
+  do {                \
+  } while (0)
+#elif defined(ASB_PROFILE)
+#define EC_WPROF_START(w) \
+  do {                    \
+  } while (0)
+#define EC_WPROF(w, k) \
+  do {                 \
+  } while (0)
 #define EC_PROF_START(w)                            \
   do {                                              \
     if (EC_LANE == 0) (w)->prof_t = ec_clock();     \
@@ -202,6 +228,12 @@ struct WS {
   } while (0)
 #define EC_PROF(w, k) \
   do {                \
+  } while (0)
+#define EC_WPROF_START(w) \
+  do {                    \
+  } while (0)
+#define EC_WPROF(w, k) \
+  do {                 \
   } while (0)
 #endif
 
@@ -1390,6 +1422,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   const AsbScenario& sc = w->sc;
   if (sc.interference > 0) return false;
   const int M = sc.n_instances;
+  EC_WPROF_START(w);
   /* ---- step 0: the rank sort already ordered exact ties by push seq; an
    * unknown seq inside a tie needs the serial walk */
   if (w->j_tie_unknown) return false;
@@ -1414,6 +1447,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   }
   if (EC_LANE == 0) w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
   t_sync();
+  EC_WPROF(w, 0);
   /* ---- step 1: per-instance replay up to the cut, in registers */
   constexpr int NPL = (64 + EC_TSIZE - 1) / EC_TSIZE; /* instances per lane */
   Inst st[NPL];
@@ -1435,6 +1469,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     first_lf = b < first_lf ? b : first_lf;
   }
   t_sync();
+  EC_WPROF(w, 1);
   /* ---- step 2: reassignment checks in order (team argmin on the snapshot) */
   int stop_p = first < first_lf ? first : first_lf;
   int stop_kind = stop_p == cut ? STOP_NONE : (first <= first_lf ? STOP_COUPLING : STOP_LOGFULL);
@@ -1468,6 +1503,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
       break;
     }
   }
+  EC_WPROF(w, 2);
   /* ---- step 3: write back per-instance state (replay again if the stop
    * lies before this lane's own replay end) */
 #pragma unroll
@@ -1482,6 +1518,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     w->in[i - 1] = st[q];
   }
   t_sync();
+  EC_WPROF(w, 3);
   /* ---- step 4: push sequence numbers, start ranks, counters (prefix scans) */
   const long long seq0 = w->seq, rank0 = w->start_ctr;
   int pushes = 0, starts = 0, turns = 0, completed = 0;
@@ -1511,6 +1548,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     starts += ec_popc(ms);
   }
   t_sync();
+  EC_WPROF(w, 4);
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
   for (int k = 0; k < n_dep; k++) {
     const int p = w->dep_pos[k];
@@ -1564,6 +1602,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     if (stop_idx >= 0) w->stop_r = w->rec[stop_idx];
   }
   t_sync();
+  EC_WPROF(w, 5);
   return true;
 }
 

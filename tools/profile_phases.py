@@ -10,7 +10,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2604_16682_b200 import _build  # noqa: E402
 
-os.environ["ASB_LIB"] = _build.build_cuda(profile=True)
+WALK = os.environ.get("ASB_PROFILE_WALK") == "1"
+os.environ["ASB_LIB"] = _build.build_cuda(profile="walk" if WALK else True)
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -20,6 +21,8 @@ from paper_2604_16682_b200 import _abi  # noqa: E402
 from paper_2604_16682_b200.engine import DeviceBatch  # noqa: E402
 
 PHASES = ("tick_sweep", "epoch_instances", "due_collect", "arrivals+speculate+sort", "walk", "apply+serial")
+if WALK:
+    PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
 
 
 def main():
