@@ -127,7 +127,8 @@ struct GP {
   int A, M, L;
 };
 
-enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5 };
+enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
+       JOB_EPOCH = 7 };
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR>
 struct WS {
@@ -147,6 +148,8 @@ struct WS {
   long long ks[RCAP];
   unsigned char kp[RCAP];
   unsigned char depflag[RCAP];
+  short ki[RCAP], kir[RCAP], krank[RCAP], ilist[RCAP]; /* per-instance record lists */
+  int icnt[MAXM], ioff[MAXM + 1];
   double now, bound;
   long long seq, start_ctr;
   long long ctr[ASB_NCOUNTERS];
@@ -165,6 +168,11 @@ struct WS {
   long long ep_uobs[MAXM], ep_seq[MAXM];
   double ep_mintp[MAXM];
   int ep_level[MAXM], ep_boost[MAXM], ep_nadm[MAXM], ep_head[MAXM], ep_retime[MAXM], ep_def[MAXM], ep_thr0[MAXM];
+  int ep_nstart[MAXM];
+  long long ep_rank[MAXM];
+  int ep_list[MAXM];
+  int n_eplist;
+  double ep_gcap;
   int due[DCAP];
   Rec rec[RCAP];
   SortE srt[RCAP];
@@ -383,15 +391,11 @@ EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
     const double t = g.next_t[a];
     add = w->incl ? t <= w->bound : t < w->bound;
   }
-  unsigned m = t_ballot(add);
   if (add) {
-    const int pos = w->n_cand + ec_popc(m & t_lt_mask());
+    const int pos = t_atomic_add_i(&w->n_cand, 1);
     if (pos < DCAP) w->due[pos] = a;
     g.dstamp[a] = w->cand_token;
   }
-  t_sync();
-  if (EC_LANE == 0) w->n_cand += ec_popc(m);
-  t_sync();
 }
 
 /* ----------------------------------------------------------------------------
@@ -403,7 +407,8 @@ EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
  * (engine.py:355-372) with push sequence numbers seq0, seq0+1, ...  Returns
  * the number of live entries (== running turns).  (team) */
 template <class W, int DCAP = 0>
-EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false) {
+EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false,
+                    bool count = true) {
   Inst& in = w->in[i - 1];
   const int len = in.log_len;
   int* lg = g.log + (long long)(i - 1) * g.A;
@@ -446,7 +451,7 @@ EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double
   }
   if (EC_LANE == 0) {
     in.log_len = out;
-    if (retime) w->ctr[ASB_CTR_RETIMES] += out;
+    if (retime && count) w->ctr[ASB_CTR_RETIMES] += out;
   }
   t_sync();
   return out;
@@ -932,26 +937,30 @@ EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, 
 
 /* β/γ FIFO admission as a prefix scan (controller.py:112-130); returns count (team) */
 template <class W>
-EC_DEV int admission(W* w, const GP& g, int i, double gcap) {
+EC_DEV int admission(W* w, const GP& g, int i, double gcap, int* n_start = nullptr) {
   Inst& in = w->in[i - 1];
   const int len = in.fifo_len, head = in.fifo_head;
   const int* ring = g.ring + (long long)(i - 1) * g.A;
+  const double now = w->now;
   long long usage = in.usage;
-  int n_adm = 0;
+  int n_adm = 0, n_st = 0;
   for (int base = 0; base < len; base += EC_TSIZE) {
     int j = base + EC_LANE;
     bool valid = j < len;
     int a = valid ? ring[ring_idx(head, j, g.A)] : -1;
     long long c = valid ? g.ctx[a] : 0;
+    const double nb = valid ? g.notbefore[a] : 0.0;
     long long incl = t_scan_add_ll(c);
     long long excl = incl - c;
     bool ok = valid && (double)(usage + excl) < gcap;
     unsigned m = t_ballot(ok);
+    n_st += ec_popc(t_ballot(ok && !(now < nb)));
     int cnt = ec_popc(m);
     if (cnt) usage += t_bcast_ll(incl, cnt - 1);
     n_adm += cnt;
     if (cnt < EC_TSIZE) break;
   }
+  if (n_start) *n_start = n_st;
   t_sync();
   if (EC_LANE == 0) {
     in.usage = usage;
@@ -994,10 +1003,10 @@ EC_DEV int choose_level(const W* w, int i, int* boosted) {
 /* start the admitted agents' turns of instance i (engine.py:458-473), no
  * interference: durations are independent, pushes numbered from seq0 (team) */
 template <class W, int DCAP>
-EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, bool collect) {
+EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, long long rank0,
+                           bool collect) {
   Inst& in = w->in[i - 1];
   if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0, 0, w->now);
-  const long long rank0 = w->start_ctr;
   const int log0 = in.log_len, lvl = in.level, thr = in.thr;
   const double now = w->now;
   int started = 0;
@@ -1037,7 +1046,6 @@ EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long 
   }
   t_sync();
   if (EC_LANE == 0) {
-    w->start_ctr += started;
     in.running += started;
     in.log_len += started;
   }
@@ -1148,25 +1156,38 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
     update_power(w, i, now);
   }
   t_sync();
-  /* (b) β/γ admission where agents are pending (team, ascending instance) */
+  /* (b) β/γ admission where agents are pending — instances in parallel, one
+   * warp each (JOB_ADMIT) */
   const bool ca = sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.thrash_avoidance;
-  const double gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
   const double bcap = (ca ? sc.beta : 1.0) * (double)sc.capacity;
-  for (int i = 1; i <= M; i++) {
-    if (w->in[i - 1].fifo_len == 0) continue;
-    int n_adm = admission(w, g, i, gcap);
-    if (EC_LANE == 0) w->ep_nadm[i - 1] = n_adm;
+  {
+    int cnt = 0;
+    for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
+      const int i = r0 + EC_LANE + 1;
+      const bool pend = i <= M && w->in[i - 1].fifo_len > 0;
+      if (i <= M) w->ep_nstart[i - 1] = 0;
+      const unsigned m = t_ballot(pend);
+      if (pend) w->ep_list[cnt + ec_popc(m & t_lt_mask())] = i;
+      cnt += ec_popc(m);
+    }
+    if (EC_LANE == 0) {
+      w->n_eplist = cnt;
+      w->ep_gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
+    }
     t_sync();
+    if (cnt) fork_job(w, JOB_ADMIT);
   }
   /* (c) lane per instance: deferral, thrash sync, rate key, push counts;
-   * exclusive scan over instances -> each instance's first push seq */
-  long long seq_base = w->seq;
+   * exclusive scans over instances -> each instance's first push seq and
+   * first start rank (the reference pushes / starts instance-major) */
+  long long seq_base = w->seq, rank_base = w->start_ctr;
   int flips = 0;
-  long long extra_retimes = 0;
+  long long extra_retimes = 0, all_retimes = 0;
+  int nwork = 0;
   for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
     const int i = r0 + EC_LANE + 1;
-    long long pushes = 0;
-    bool flip = false;
+    long long pushes = 0, starts = 0;
+    bool flip = false, work = false;
     if (i <= M) {
       Inst& in = w->in[i - 1];
       w->ep_def[i - 1] = (double)in.usage > bcap;
@@ -1186,31 +1207,38 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
       const int rt = (changed1 || changed2) && in.running > 0 ? in.running : 0;
       w->ep_retime[i - 1] = rt;
       extra_retimes += (changed1 && changed2) ? rt : 0;
+      all_retimes += rt;
       pushes = rt + w->ep_nadm[i - 1];
+      starts = w->ep_nstart[i - 1];
+      work = pushes > 0;
     }
     flips += ec_popc(t_ballot(flip));
-    long long incl = t_scan_add_ll(pushes);
-    if (i <= M) w->ep_seq[i - 1] = seq_base + incl - pushes;
+    const long long incl = t_scan_add_ll(pushes);
+    const long long incs = t_scan_add_ll(starts);
+    if (i <= M) {
+      w->ep_seq[i - 1] = seq_base + incl - pushes;
+      w->ep_rank[i - 1] = rank_base + incs - starts;
+    }
     seq_base += t_bcast_ll(incl, EC_TSIZE - 1);
+    rank_base += t_bcast_ll(incs, EC_TSIZE - 1);
+    const unsigned m = t_ballot(work);
+    if (work) w->ep_list[nwork + ec_popc(m & t_lt_mask())] = i;
+    nwork += ec_popc(m);
   }
-  t_sync();
   extra_retimes = t_sum_ll(extra_retimes);
+  all_retimes = t_sum_ll(all_retimes);
+  t_sync();
   if (EC_LANE == 0) {
     w->seq = seq_base;
+    w->start_ctr = rank_base;
     w->ctr[ASB_CTR_THRASH_FLIPS] += flips;
-    w->ctr[ASB_CTR_RETIMES] += extra_retimes;
+    w->ctr[ASB_CTR_RETIMES] += all_retimes + extra_retimes;
+    w->n_eplist = nwork;
   }
-  /* (d) re-time in-flight turns where the rate key changed (team) */
-  for (int i = 1; i <= M; i++) {
-    if (!w->ep_retime[i - 1]) continue;
-    log_pass<W, DCAP>(w, g, i, 1, w->ep_seq[i - 1], now, true);
-  }
-  /* (e) start admitted turns, ascending instance (start ranks are global) */
-  for (int i = 1; i <= M; i++) {
-    const int n_adm = w->ep_nadm[i - 1];
-    if (!n_adm) continue;
-    start_admitted<W, DCAP>(w, g, i, w->ep_head[i - 1], n_adm, w->ep_seq[i - 1] + w->ep_retime[i - 1], true);
-  }
+  t_sync();
+  /* (d)+(e) re-time in-flight turns where the rate key changed, then start
+   * the admitted turns — instances in parallel, one warp each (JOB_EPOCH) */
+  if (nwork) fork_job(w, JOB_EPOCH);
   /* (f) lane per instance: final power, decision rows */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     update_power(w, i, now);
@@ -1358,30 +1386,42 @@ EC_DEV void walk_serial(W* w, const GP& g, const int n) {
   t_sync();
 }
 
-/* Per-instance replay of the sorted records [0, end) for instance i, in
- * registers: usage, running count, running log, power.  Stops before the
- * first thrash flip / log overflow (returned in *flip / *lf).  If `snap`,
- * records the usage before every dependent record.  (one lane) */
+/* register state of one instance during the commit walk */
+struct RS {
+  long long usage;
+  int running, log_len;
+  double watts, t_pow, energy;
+};
+
+/* Per-instance replay of instance i's records (its sorted list) with
+ * position < end, in registers: usage, running count, running log, power.
+ * Stops before the first thrash flip / log overflow (position returned in
+ * *flip / *lf).  If `snap`, records the usage before every dependent record.
+ * Returns the position processing stopped at (end if none).  (one lane) */
 template <class W>
-EC_DEV int replay_instance(W* w, const GP& g, int i, int end, bool snap, int* flip, int* lf, Inst& st) {
+EC_DEV int replay_list(W* w, const GP& g, int i, int end, bool snap, int* flip, int* lf, RS& st) {
+  const Inst& in = w->in[i - 1];
   const long long cap = w->sc.capacity;
-  const int thr = st.thr;
-  const double act = w->act[st.level - 1], idle = w->idle[st.level - 1];
+  const int thr = in.thr;
+  const double act = w->act[in.level - 1], idle = w->idle[in.level - 1];
+  const int nd = snap ? w->n_dep : 0;
   int kk = 0;
-  int dp = (snap && w->n_dep > 0) ? w->dep_pos[0] : 0x7fffffff;
-  int p = 0;
-  for (; p < end; p++) {
-    if (dp == p) {
+  int dp = nd > 0 ? w->dep_pos[0] : 0x7fffffff;
+  const int k1 = w->ioff[i];
+  int stopped = end;
+  for (int k = w->ioff[i - 1]; k < k1; k++) {
+    const int p = w->ilist[k];
+    if (p >= end) break;
+    while (dp <= p) {
       w->snap[kk][i - 1] = st.usage;
       kk++;
-      dp = kk < w->n_dep ? w->dep_pos[kk] : 0x7fffffff;
+      dp = kk < nd ? w->dep_pos[kk] : 0x7fffffff;
     }
-    if (w->sw_inst[p] != i) continue;
-    const int pr = w->sw_prio[p];
-    if (pr == EV_COMPLETE) {
-      long long nu = st.usage + w->sw_du[p];
+    if (w->sw_prio[p] == EV_COMPLETE) {
+      const long long nu = st.usage + w->sw_du[p];
       if ((nu > cap ? 1 : 0) != thr) {
         *flip = p;
+        stopped = p;
         break;
       }
       st.usage = nu;
@@ -1389,6 +1429,7 @@ EC_DEV int replay_instance(W* w, const GP& g, int i, int end, bool snap, int* fl
     } else {
       if (st.log_len >= g.A) {
         *lf = p;
+        stopped = p;
         break;
       }
       Rec& r = w->rec[w->sw_idx[p]];
@@ -1405,7 +1446,34 @@ EC_DEV int replay_instance(W* w, const GP& g, int i, int end, bool snap, int* fl
       st.watts = wt;
     }
   }
-  return p;
+  while (dp < stopped) {
+    w->snap[kk][i - 1] = st.usage;
+    kk++;
+    dp = kk < nd ? w->dep_pos[kk] : 0x7fffffff;
+  }
+  return stopped;
+}
+
+template <class W>
+EC_DEV void rs_load(const W* w, int i, RS& st) {
+  const Inst& in = w->in[i - 1];
+  st.usage = in.usage;
+  st.running = in.running;
+  st.log_len = in.log_len;
+  st.watts = in.watts;
+  st.t_pow = in.t_pow;
+  st.energy = in.energy;
+}
+
+template <class W>
+EC_DEV void rs_store(W* w, int i, const RS& st) {
+  Inst& in = w->in[i - 1];
+  in.usage = st.usage;
+  in.running = st.running;
+  in.log_len = st.log_len;
+  in.watts = st.watts;
+  in.t_pow = st.t_pow;
+  in.energy = st.energy;
 }
 
 /* Parallel commit walk (team).  The serial walk's state machine decomposes
@@ -1448,20 +1516,28 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   if (EC_LANE == 0) w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
   t_sync();
   EC_WPROF(w, 0);
-  /* ---- step 1: per-instance replay up to the cut, in registers */
-  constexpr int NPL = (64 + EC_TSIZE - 1) / EC_TSIZE; /* instances per lane */
-  Inst st[NPL];
-  int endp[NPL];
+  /* ---- step 1: per-instance replay up to the cut, in registers (lane
+   * i-1 owns instance i; instances 33..64 are replayed in step 3) */
+  RS st0;
+  int end0 = cut;
   int first = cut, first_lf = cut;
-#pragma unroll
-  for (int q = 0; q < NPL; q++) {
-    const int i = EC_LANE + 1 + q * EC_TSIZE;
-    if (i > M) break;
-    st[q] = w->in[i - 1];
-    int f = cut, l = cut;
-    endp[q] = replay_instance(w, g, i, cut, true, &f, &l, st[q]);
-    first = f < first ? f : first;
-    first_lf = l < first_lf ? l : first_lf;
+  {
+    const int i0 = EC_LANE + 1;
+    if (i0 <= M) {
+      rs_load(w, i0, st0);
+      int f = cut, l = cut;
+      end0 = replay_list(w, g, i0, cut, true, &f, &l, st0);
+      first = f;
+      first_lf = l;
+    }
+    for (int i = EC_LANE + 1 + EC_TSIZE; i <= M; i += EC_TSIZE) {
+      RS t;
+      rs_load(w, i, t);
+      int f = cut, l = cut;
+      replay_list(w, g, i, cut, true, &f, &l, t);
+      first = f < first ? f : first;
+      first_lf = l < first_lf ? l : first_lf;
+    }
   }
   for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
     int a = t_shfl_xor_i(first, o), b = t_shfl_xor_i(first_lf, o);
@@ -1506,16 +1582,23 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
   EC_WPROF(w, 2);
   /* ---- step 3: write back per-instance state (replay again if the stop
    * lies before this lane's own replay end) */
-#pragma unroll
-  for (int q = 0; q < NPL; q++) {
-    const int i = EC_LANE + 1 + q * EC_TSIZE;
-    if (i > M) break;
-    if (endp[q] != stop_p) {
-      st[q] = w->in[i - 1];
-      int f = stop_p, l = stop_p;
-      replay_instance(w, g, i, stop_p, false, &f, &l, st[q]);
+  {
+    const int i0 = EC_LANE + 1;
+    if (i0 <= M) {
+      if (end0 != stop_p) {
+        rs_load(w, i0, st0);
+        int f = stop_p, l = stop_p;
+        replay_list(w, g, i0, stop_p, false, &f, &l, st0);
+      }
+      rs_store(w, i0, st0);
     }
-    w->in[i - 1] = st[q];
+    for (int i = EC_LANE + 1 + EC_TSIZE; i <= M; i += EC_TSIZE) {
+      RS t;
+      rs_load(w, i, t);
+      int f = stop_p, l = stop_p;
+      replay_list(w, g, i, stop_p, false, &f, &l, t);
+      rs_store(w, i, t);
+    }
   }
   t_sync();
   EC_WPROF(w, 3);
@@ -1666,12 +1749,15 @@ EC_DEV void job_spec(W* w, const GP& g, int tid, int nthr) {
 template <class W>
 EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
+  const int M = w->sc.n_instances;
+  for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
   for (int j = tid; j < n_all; j += nthr) {
     const Rec& r = w->rec[j];
     const bool empty = r.flags & F_EMPTY;
     w->kt[j] = empty ? ~0ull : ec_bits(r.t);
     w->kp[j] = empty ? 0xff : (unsigned char)r.prio;
     w->ks[j] = r.seq;
+    w->ki[j] = (short)(empty || r.prio == EV_ARRIVAL ? 0 : r.inst);
   }
   ec_team_barrier();
   int tie_unknown = 0;
@@ -1680,18 +1766,27 @@ EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
     const unsigned long long tj = w->kt[j];
     const unsigned pj = w->kp[j];
     const long long sj = w->ks[j];
-    int rank = 0;
+    const int ij = w->ki[j];
+    int rank = 0, irank = 0;
     for (int q = 0; q < n_all; q++) {
       const unsigned long long tq = w->kt[q];
       const unsigned pq = w->kp[q];
+      bool less = false;
       if (tq < tj || (tq == tj && pq < pj)) {
-        rank++;
+        less = true;
       } else if (tq == tj && pq == pj && q != j) {
         const long long sq = w->ks[q];
         if (sq < 0 || sj < 0) tie_unknown = 1;
-        if (sq < sj || (sq == sj && q < j)) rank++;
+        less = sq < sj || (sq == sj && q < j);
+      }
+      if (less) {
+        rank++;
+        if (w->ki[q] == ij) irank++;
       }
     }
+    w->krank[j] = (short)rank;
+    w->kir[j] = (short)irank;
+    if (ij) t_atomic_add_i(&w->icnt[ij - 1], 1);
     const Rec& r = w->rec[j];
     SortE& e = w->srt[rank];
     e.tb = tj;
@@ -1707,6 +1802,23 @@ EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (!below_horizon(tj, pj, sj, w->hz_t, (unsigned)w->hz_p, w->hz_s)) t_atomic_min_i(&w->j_cut, rank);
   }
   if (tie_unknown) w->j_tie_unknown = 1;
+  ec_team_barrier();
+  if (tid < EC_TSIZE) { /* warp 0: exclusive scan of the per-instance record counts */
+    long long run = 0;
+    for (int base = 0; base < M; base += EC_TSIZE) {
+      const int i = base + EC_LANE;
+      const long long c = i < M ? w->icnt[i] : 0;
+      const long long inc = t_scan_add_ll(c);
+      if (i < M) w->ioff[i] = (int)(run + inc - c);
+      run += t_bcast_ll(inc, EC_TSIZE - 1);
+    }
+    if (EC_LANE == 0) w->ioff[M] = (int)run;
+  }
+  ec_team_barrier();
+  for (int j = tid; j < n_all; j += nthr) {
+    const int ij = w->ki[j];
+    if (ij && w->kp[j] != 0xff) w->ilist[w->ioff[ij - 1] + w->kir[j]] = w->krank[j];
+  }
 }
 
 /* JOB_APPLY (thread-level): write back every due agent's committed chain
@@ -1800,6 +1912,37 @@ EC_DEV void job_init(W* w, const GP& g, int tid, int nthr) {
   }
 }
 
+/* JOB_ADMIT (warp per instance): β/γ admission of the listed instances */
+template <class W>
+EC_DEV void job_admit(W* w, const GP& g, int tid, int nthr) {
+  const int warp = tid / EC_TSIZE, nwarps = nthr >= EC_TSIZE ? nthr / EC_TSIZE : 1;
+  for (int k = warp; k < w->n_eplist; k += nwarps) {
+    const int i = w->ep_list[k];
+    int n_start = 0;
+    const int n_adm = admission(w, g, i, w->ep_gcap, &n_start);
+    if (EC_LANE == 0) {
+      w->ep_nadm[i - 1] = n_adm;
+      w->ep_nstart[i - 1] = n_start;
+    }
+  }
+}
+
+/* JOB_EPOCH (warp per instance): re-time and start admitted turns of the
+ * listed instances with their precomputed push seq / start rank bases */
+template <class W>
+EC_DEV void job_epoch(W* w, const GP& g, int tid, int nthr) {
+  const int warp = tid / EC_TSIZE, nwarps = nthr >= EC_TSIZE ? nthr / EC_TSIZE : 1;
+  const double now = w->now;
+  for (int k = warp; k < w->n_eplist; k += nwarps) {
+    const int i = w->ep_list[k];
+    const int rt = w->ep_retime[i - 1];
+    if (rt) log_pass<W, W::DC>(w, g, i, 1, w->ep_seq[i - 1], now, true, false);
+    const int n_adm = w->ep_nadm[i - 1];
+    if (n_adm)
+      start_admitted<W, W::DC>(w, g, i, w->ep_head[i - 1], n_adm, w->ep_seq[i - 1] + rt, w->ep_rank[i - 1], true);
+  }
+}
+
 template <class W>
 EC_DEV void do_job(W* w, int job, int tid, int nthr) {
   const GP& g = w->gp;
@@ -1809,6 +1952,8 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
     case JOB_SPEC: job_spec(w, g, tid, nthr); break;
     case JOB_SORT: job_sort(w, g, tid, nthr); break;
     case JOB_APPLY: job_apply(w, g, tid, nthr); break;
+    case JOB_ADMIT: job_admit(w, g, tid, nthr); break;
+    case JOB_EPOCH: job_epoch(w, g, tid, nthr); break;
     default: break;
   }
 }
