@@ -311,8 +311,8 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
   if (max_instances <= 16)
-    return launch_engine<16, 256, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
-  return launch_engine<64, 256, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
+    return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
+  return launch_engine<64, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
 }
 
 }  // extern "C"
