@@ -251,6 +251,7 @@ def main():
 
     from paper_2604_16682_b200 import _abi, _build
     from paper_2604_16682_b200.engine import DeviceBatch
+    from paper_2604_16682_b200.parallel import allreduce_stats
 
     _build.build_cuda()
     torch.cuda.set_device(local)
@@ -275,7 +276,7 @@ def main():
         torch.ops.agentsim_b200.scenario_stats(db.scen, db.out_list, db.stats)
         torch.ops.agentsim_b200.reduce_stats(db.stats, db.outputs["counters"], batch.n, db.red)
         if pg is not None:
-            pg.all_reduce(db.red)
+            allreduce_stats(db.red)
 
     for _ in range(max(args.warmup, 0)):
         step()
