@@ -82,7 +82,8 @@ enum {
   ASB_SIMERR_NONE = 0,
   ASB_SIMERR_INVARIANT = 1, /* state-machine misuse (SimulationError) */
   ASB_SIMERR_OVERFLOW = 2,  /* a bounded engine buffer overflowed */
-  ASB_SIMERR_ORDER = 3      /* an event was scheduled before its parent */
+  ASB_SIMERR_ORDER = 3,     /* an event was scheduled before its parent */
+  ASB_SIMERR_LIVELOCK = 4   /* engine watchdog: a window made no progress */
 };
 
 /* One scenario = one SimConfig (engine.py:57-88) bound to a trace. 8-byte aligned. */

@@ -29,7 +29,8 @@ RED = ("energy", "thrash_fraction_sum", "completed", "slo_met", "ticks", "thrash
 VARIANTS = {"context_aware": 0, "off": 1, "fixed": 2}
 POLICIES = {"context_aware": 0, "round_robin": 1, "least_loaded": 2}
 PHASES = ("arriving", "pending", "running", "tool", "waiting_start", "done")
-SIMERR = {0: "ok", 1: "invariant violation", 2: "engine buffer overflow", 3: "event scheduled before its parent"}
+SIMERR = {0: "ok", 1: "invariant violation", 2: "engine buffer overflow", 3: "event scheduled before its parent",
+          4: "engine watchdog (no progress inside a window)"}
 
 SCENARIO_DTYPE = np.dtype(
     [

@@ -21,6 +21,7 @@ LIB_DIR = os.path.join(PKG, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200.so")
 PROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_prof.so")
 WPROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_wprof.so")
+DEBUG_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_debug.so")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "build", "liboracle.so")
 HOST_ENGINE_LIB = os.path.join(ROOT, "tests", "native", "build", "libhost_engine.so")
 
@@ -54,11 +55,14 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
     (-DASB_PROFILE, counters[10..15]) used only by tools/profile_phases.py."""
     srcs = [os.path.join(CSRC, f) for f in ("engine.cu", "unit_ops.cu")]
     deps = srcs + [os.path.join(CSRC, "engine_core.h"), os.path.join(ROOT, "include", "agentsim_b200.h")]
-    target = WPROF_LIB_PATH if profile == "walk" else (PROF_LIB_PATH if profile else LIB_PATH)
+    target = {"walk": WPROF_LIB_PATH, "debug": DEBUG_LIB_PATH}.get(profile) if isinstance(profile, str) else (
+        PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
         cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", target + ".tmp", *srcs]
-        if profile:
+        if profile == "debug":
+            cmd.insert(1, "-DASB_DEBUG_TRACE")
+        elif profile:
             cmd.insert(1, "-DASB_PROFILE")
         if profile == "walk":
             cmd.insert(1, "-DASB_PROFILE_WALK")

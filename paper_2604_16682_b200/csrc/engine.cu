@@ -18,6 +18,25 @@
 
 #define FULLMASK 0xffffffffu
 #define EC_DEV __device__ __forceinline__
+#ifndef ASB_COLD_MASK
+#define ASB_COLD_MASK 7
+#endif
+#define EC_COLD __device__ __noinline__
+#if ASB_COLD_MASK & 1
+#define EC_COLD1 __device__ __noinline__
+#else
+#define EC_COLD1 __device__ __forceinline__
+#endif
+#if ASB_COLD_MASK & 2
+#define EC_COLD2 __device__ __noinline__
+#else
+#define EC_COLD2 __device__ __forceinline__
+#endif
+#if ASB_COLD_MASK & 4
+#define EC_COLD3 __device__ __noinline__
+#else
+#define EC_COLD3 __device__ __forceinline__
+#endif
 #define EC_LANE ((int)(threadIdx.x & 31))
 #define EC_TSIZE 32
 #define EC_NAN __longlong_as_double(0x7ff8000000000000ll)
@@ -57,9 +76,9 @@ EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__doubl
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 EC_DEV long long ec_clock() { return clock64(); }
 #define EC_TID ((int)threadIdx.x)
-EC_DEV void ec_fork_begin(int nt) { asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory"); }
-EC_DEV void ec_fork_end(int nt) { asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory"); }
-EC_DEV void ec_team_barrier() { asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory"); }
+EC_DEV void ec_fork_begin(int nt) { asm volatile("barrier.sync 1, %0;" ::"r"(nt) : "memory"); }
+EC_DEV void ec_fork_end(int nt) { asm volatile("barrier.sync 2, %0;" ::"r"(nt) : "memory"); }
+EC_DEV void ec_team_barrier() { asm volatile("barrier.sync 3, %0;" ::"r"((int)blockDim.x) : "memory"); }
 EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
 EC_DEV unsigned long long t_warp_min_ull(unsigned long long v) {
 #pragma unroll
@@ -81,6 +100,20 @@ EC_DEV void t_warp_min_key(unsigned long long& t, unsigned& p) {
     }
   }
 }
+
+#ifdef ASB_DEBUG_TRACE
+__device__ long long* volatile g_asb_dbg;
+#define EC_DBG(slot, value)                                                 \
+  do {                                                                      \
+    long long* d_ = g_asb_dbg;                                              \
+    if (d_ && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                 \
+      ((volatile long long*)d_)[(slot)] = (long long)(value);               \
+      ((volatile long long*)d_)[32 + (slot)] += 1;                          \
+      ((volatile long long*)d_)[63] = (long long)(slot) | ((long long)threadIdx.x << 32); \
+      __threadfence_system();                                               \
+    }                                                                       \
+  } while (0)
+#endif
 
 #include "engine_core.h"
 
@@ -293,6 +326,13 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
 extern "C" {
 
 int asb_abi_version(void) { return ASB_ABI_VERSION; }
+
+#ifdef ASB_DEBUG_TRACE
+/* debug builds only: host-mapped long long[64] progress markers (block 0) */
+int asb_debug_trace(void* host_mapped) {
+  return cudaMemcpyToSymbol(g_asb_dbg, &host_mapped, sizeof(void*)) == cudaSuccess ? 0 : -2;
+}
+#endif
 
 size_t asb_workspace_bytes(int32_t n_scen, int64_t total_agents, int64_t total_ring_slots) {
   return carve(nullptr, n_scen, total_agents, total_ring_slots, nullptr);

@@ -50,6 +50,36 @@
  *   ec_from_bits, ec_clock, EC_NAN, EC_INF, EC_INF_BITS
  */
 
+/* EC_COLD: large phase functions, kept out of line so the hot loops stay
+ * inside the instruction cache (includer may override) */
+#ifndef EC_COLD
+#define EC_COLD EC_DEV
+#endif
+#ifndef EC_COLD1
+#define EC_COLD1 EC_COLD /* fork-join job bodies */
+#endif
+#ifndef EC_COLD2
+#define EC_COLD2 EC_COLD /* serial handlers */
+#endif
+#ifndef EC_COLD3
+#define EC_COLD3 EC_COLD /* epoch / batch phases */
+#endif
+
+/* EC_LANE0 { ... }: a lane-0 section of the main warp's serial code.  Lanes
+ * of a warp are independently scheduled, so every lane must have read the
+ * shared state it needs before lane 0 starts mutating it: the section opens
+ * with a warp barrier (and every section is followed by one, so the other
+ * lanes read lane 0's results only after it finished). */
+#define EC_LANE0 if ((t_sync(), EC_LANE == 0))
+
+/* EC_DBG(slot, value): progress markers for hang debugging (GPU debug build
+ * -DASB_DEBUG_TRACE writes them to host-mapped memory); no-op otherwise */
+#ifndef EC_DBG
+#define EC_DBG(slot, value) \
+  do {                      \
+  } while (0)
+#endif
+
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
 #endif
@@ -407,14 +437,16 @@ EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
  * (engine.py:355-372) with push sequence numbers seq0, seq0+1, ...  Returns
  * the number of live entries (== running turns).  (team) */
 template <class W, int DCAP = 0>
-EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false,
+EC_COLD2 int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false,
                     bool count = true) {
   Inst& in = w->in[i - 1];
   const int len = in.log_len;
   int* lg = g.log + (long long)(i - 1) * g.A;
   const int level = in.level, running = in.running, thr = in.thr;
   int out = 0;
+  EC_DBG(9, len);
   for (int base = 0; base < len; base += EC_TSIZE) {
+    EC_DBG(10, base);
     int p = base + EC_LANE;
     int a = -1;
     bool live = false;
@@ -449,7 +481,7 @@ EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double
     t_sync();
     if (DCAP > 0 && collect) add_candidates<W, DCAP>(w, g, live ? a : -1, retime && live);
   }
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     in.log_len = out;
     if (retime && count) w->ctr[ASB_CTR_RETIMES] += out;
   }
@@ -459,8 +491,8 @@ EC_DEV int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double
 
 /* _conditions_changed, engine.py:344-372 (team, serial context: uses w->seq) */
 template <class W>
-EC_DEV void cond_changed(W* w, const GP& g, int i) {
-  if (EC_LANE == 0) {
+EC_COLD2 void cond_changed(W* w, const GP& g, int i) {
+  EC_LANE0 {
     Inst& in = w->in[i - 1];
     int kr = w->sc.interference > 0 ? in.running : 0;
     int changed = !(in.key_valid && in.key_level == in.level && in.key_thr == in.thr && in.key_run == kr);
@@ -475,7 +507,7 @@ EC_DEV void cond_changed(W* w, const GP& g, int i) {
   t_sync();
   if (w->flag) {
     int cnt = log_pass(w, g, i, 1, w->seq, w->now);
-    if (EC_LANE == 0) w->seq += cnt;
+    EC_LANE0 w->seq += cnt;
     t_sync();
   }
 }
@@ -502,12 +534,14 @@ EC_DEV void count_flip(W* w, int i, double now) {
 
 /* _start_turn, engine.py:374-401 */
 template <class W>
-EC_DEV void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
-  if (EC_LANE == 0) w->in[i - 1].running += 1;
+EC_COLD2 void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
+  EC_LANE0 w->in[i - 1].running += 1;
   t_sync();
   cond_changed(w, g, i);
-  if (w->in[i - 1].log_len >= g.A) log_pass(w, g, i, 0, 0, w->now);
-  if (EC_LANE == 0) {
+  const bool full = w->in[i - 1].log_len >= g.A;
+  t_sync(); /* every lane has read log_len before lane 0 appends */
+  if (full) log_pass(w, g, i, 0, 0, w->now);
+  EC_LANE0 {
     Inst& in = w->in[i - 1];
     double now = w->now;
     long long turn = g.aturn[a] + g.steps[a];
@@ -527,9 +561,9 @@ EC_DEV void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
 
 /* _on_complete, engine.py:509-535 */
 template <class W>
-EC_DEV void complete_serial(W* w, const GP& g, int a) {
+EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
   int i = g.inst[a];
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     Inst& in = w->in[i - 1];
     double now = w->now;
     in.running -= 1;
@@ -571,15 +605,16 @@ EC_DEV void complete_serial(W* w, const GP& g, int a) {
   }
   t_sync();
   cond_changed(w, g, i);
-  if (EC_LANE == 0) update_power(w, i, w->now);
+  EC_LANE0 update_power(w, i, w->now);
   t_sync();
 }
 
 /* _on_tool, engine.py:537-561 */
 template <class W>
-EC_DEV void tool_serial(W* w, const GP& g, int a) {
+EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
   int source = g.inst[a];
-  if (EC_LANE == 0) {
+  t_sync(); /* every lane has read the source before lane 0 migrates the agent */
+  EC_LANE0 {
     int target = 0;
     w->ctr[ASB_CTR_EVENTS]++;
     if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
@@ -616,20 +651,21 @@ EC_DEV void tool_serial(W* w, const GP& g, int a) {
     return;
   }
   cond_changed(w, g, source);
-  if (EC_LANE == 0) update_power(w, source, w->now);
+  EC_LANE0 update_power(w, source, w->now);
   t_sync();
 }
 
 template <class W>
-EC_DEV void exec_serial(W* w, const GP& g, const Rec& r) {
-  if (EC_LANE == 0) w->now = r.t;
+EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
+  EC_DBG(7, r.prio * 1000000 + r.agent);
+  EC_LANE0 w->now = r.t;
   t_sync();
   if (r.prio == EV_COMPLETE) {
     complete_serial(w, g, r.agent);
   } else if (r.prio == EV_TOOL) {
     tool_serial(w, g, r.agent);
   } else {
-    if (EC_LANE == 0) w->ctr[ASB_CTR_EVENTS]++;
+    EC_LANE0 w->ctr[ASB_CTR_EVENTS]++;
     t_sync();
     start_turn_serial(w, g, g.inst[r.agent], r.agent, g.issue[r.agent]);
   }
@@ -786,7 +822,7 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr);
  * job simply runs on the single lane.) */
 template <class W>
 EC_DEV void fork_job(W* w, int job) {
-  if (EC_LANE == 0) w->job = job;
+  EC_LANE0 w->job = job;
   t_sync();
   ec_fork_begin(W::NT);
   do_job(w, job, EC_TID, W::NT);
@@ -810,7 +846,7 @@ EC_DEV void helper_loop(W* w) {
  * whose next event falls before j_bound become due candidates (stamped
  * j_token). */
 template <class W>
-EC_DEV void job_sweep(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
   const int M = w->sc.n_instances;
   const bool tick = w->j_tick, collect = w->j_collect;
@@ -875,10 +911,10 @@ EC_DEV void job_sweep(W* w, const GP& g, int tid, int nthr) {
  * minima into tmin (controller.py:89-103, engine.py:437-454), count the
  * ticks, and compact finished agents out lazily. */
 template <class W>
-EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
+EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
   const int M = w->sc.n_instances;
   const int n = w->n_alive;
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->j_tick = 1;
     w->j_collect = collect;
     w->j_bound = bound;
@@ -897,7 +933,7 @@ EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, 
     w->tmin[i] = mn;
   }
   const int dead_all = w->j_dead;
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->ctr[ASB_CTR_TICKS] += n - dead_all;
     w->n_cand = collect ? w->j_total : 0;
     w->cand_token = token;
@@ -930,14 +966,14 @@ EC_DEV void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, 
       out += ec_popc(m);
       t_sync();
     }
-    if (EC_LANE == 0) w->n_alive = out;
+    EC_LANE0 w->n_alive = out;
   }
   t_sync();
 }
 
 /* β/γ FIFO admission as a prefix scan (controller.py:112-130); returns count (team) */
 template <class W>
-EC_DEV int admission(W* w, const GP& g, int i, double gcap, int* n_start = nullptr) {
+EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nullptr) {
   Inst& in = w->in[i - 1];
   const int len = in.fifo_len, head = in.fifo_head;
   const int* ring = g.ring + (long long)(i - 1) * g.A;
@@ -962,7 +998,7 @@ EC_DEV int admission(W* w, const GP& g, int i, double gcap, int* n_start = nullp
   }
   if (n_start) *n_start = n_st;
   t_sync();
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     in.usage = usage;
     in.fifo_head = ring_idx(head, n_adm, g.A);
     in.fifo_len = len - n_adm;
@@ -1003,7 +1039,7 @@ EC_DEV int choose_level(const W* w, int i, int* boosted) {
 /* start the admitted agents' turns of instance i (engine.py:458-473), no
  * interference: durations are independent, pushes numbered from seq0 (team) */
 template <class W, int DCAP>
-EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, long long rank0,
+EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, long long rank0,
                            bool collect) {
   Inst& in = w->in[i - 1];
   if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0, 0, w->now);
@@ -1045,7 +1081,7 @@ EC_DEV void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long 
     if (collect) add_candidates<W, DCAP>(w, g, a, valid);
   }
   t_sync();
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     in.running += started;
     in.log_len += started;
   }
@@ -1070,12 +1106,13 @@ EC_DEV void write_decision(W* w, const GP& g, long long k, int i) {
 
 /* exact serial epoch (interference mode: every start re-times its instance) */
 template <class W>
-EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
+EC_COLD2 void epoch_serial(W* w, const GP& g, long long k) {
+  EC_DBG(8, k);
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances;
   for (int i = 1; i <= M; i++) {
     Inst& in = w->in[i - 1];
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       int boosted;
       w->ep_uobs[i - 1] = in.usage;
       in.level = w->ep_level[i - 1] = choose_level(w, i, &boosted);
@@ -1083,7 +1120,7 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
     }
     t_sync();
     cond_changed(w, g, i);
-    if (EC_LANE == 0) update_power(w, i, w->now);
+    EC_LANE0 update_power(w, i, w->now);
     t_sync();
     double gamma = 1.0, beta = 1.0;
     if (sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.thrash_avoidance) {
@@ -1092,7 +1129,7 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
     }
     const int head0 = in.fifo_head;
     const int n_adm = admission(w, g, i, gamma * (double)sc.capacity);
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       w->ep_nadm[i - 1] = n_adm;
       w->ep_def[i - 1] = (double)in.usage > beta * (double)sc.capacity;
       count_flip(w, i, w->now);
@@ -1104,9 +1141,9 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
       double issue = ec_isnan(g.pissue[a]) ? w->now : g.pissue[a];
       const bool wait = w->now < g.notbefore[a];
       t_sync();
-      if (EC_LANE == 0) g.pissue[a] = EC_NAN;
+      EC_LANE0 g.pissue[a] = EC_NAN;
       if (wait) {
-        if (EC_LANE == 0) {
+        EC_LANE0 {
           g.phase[a] = ASB_PHASE_WAITING_START;
           g.issue[a] = issue;
           set_event(g, a, i, EV_ISSUE, g.notbefore[a], w->seq++);
@@ -1116,7 +1153,7 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
         start_turn_serial(w, g, i, a, issue);
       }
     }
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       update_power(w, i, w->now);
       write_decision(w, g, k, i);
     }
@@ -1128,7 +1165,7 @@ EC_DEV void epoch_serial(W* w, const GP& g, long long k) {
  * Instances are independent within an epoch except for the instance-major
  * order of their pushes, which an exclusive scan reproduces. */
 template <class W, int DCAP>
-EC_DEV void epoch_event(W* w, const GP& g, long long k) {
+EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances;
   const bool collect = sc.interference == 0;
@@ -1137,7 +1174,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   EC_PROF(w, 0);
   if (!collect) {
     epoch_serial(w, g, k);
-    if (EC_LANE == 0) w->due_ready = 0;
+    EC_LANE0 w->due_ready = 0;
     t_sync();
     EC_PROF(w, 1);
     return;
@@ -1170,7 +1207,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
       if (pend) w->ep_list[cnt + ec_popc(m & t_lt_mask())] = i;
       cnt += ec_popc(m);
     }
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       w->n_eplist = cnt;
       w->ep_gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
     }
@@ -1228,7 +1265,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
   extra_retimes = t_sum_ll(extra_retimes);
   all_retimes = t_sum_ll(all_retimes);
   t_sync();
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->seq = seq_base;
     w->start_ctr = rank_base;
     w->ctr[ASB_CTR_THRASH_FLIPS] += flips;
@@ -1244,7 +1281,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
     update_power(w, i, now);
     write_decision(w, g, k, i);
   }
-  if (EC_LANE == 0) w->due_ready = w->n_cand <= DCAP;
+  EC_LANE0 w->due_ready = w->n_cand <= DCAP;
   t_sync();
   EC_PROF(w, 1);
 }
@@ -1255,7 +1292,7 @@ EC_DEV void epoch_event(W* w, const GP& g, long long k) {
 
 /* count alive agents whose next event is due before `bound` (team) */
 template <class W>
-EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
+EC_COLD3 int count_due(const W* w, const GP& g, double bound, int incl) {
   constexpr int U = EC_SWEEP_UNROLL;
   int c = 0;
   const int n = w->n_alive;
@@ -1279,7 +1316,7 @@ EC_DEV int count_due(const W* w, const GP& g, double bound, int incl) {
  * (> DCAP means the list is incomplete).  (main warp; forks the sweep) */
 template <class W, int DCAP>
 EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->j_tick = 0;
     w->j_collect = 1;
     w->j_bound = bound;
@@ -1295,8 +1332,8 @@ EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
  * order, stopping before the first coupling event.  Used for interference
  * mode and for tie groups whose push order is only known during the walk. */
 template <class W>
-EC_DEV void walk_serial(W* w, const GP& g, const int n) {
-  if (EC_LANE == 0) {
+EC_COLD2 void walk_serial(W* w, const GP& g, const int n) {
+  EC_LANE0 {
     const AsbScenario& sc = w->sc;
     int stop = STOP_NONE, stop_idx = -1;
     int p = 0;
@@ -1486,7 +1523,7 @@ EC_DEV void rs_store(W* w, int i, const RS& st) {
  * walk_serial) under interference or when a tie group contains a record
  * whose push order is only known during the walk. */
 template <class W, int RCAP>
-EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
+EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   const AsbScenario& sc = w->sc;
   if (sc.interference > 0) return false;
   const int M = sc.n_instances;
@@ -1513,7 +1550,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
     int oc = t_shfl_xor_i(cut, o);
     cut = oc < cut ? oc : cut;
   }
-  if (EC_LANE == 0) w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
+  EC_LANE0 w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
   t_sync();
   EC_WPROF(w, 0);
   /* ---- step 1: per-instance replay up to the cut, in registers (lane
@@ -1664,14 +1701,14 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
       }
       target = light != 0x7fffffff ? light : bi;
     }
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       const Rec& r = w->rec[w->sw_idx[p]];
       if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
       commit_arrival(w, g, r.agent, target, (int)r.seq);
     }
     t_sync();
   }
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->seq += pushes;
     w->start_ctr += starts;
     w->ctr[ASB_CTR_TURNS] += turns;
@@ -1693,7 +1730,7 @@ EC_DEV bool walk_parallel(W* w, const GP& g, const int n) {
  * chains inside the window; continuation records are allocated atomically;
  * the smallest dropped key becomes the batch horizon. */
 template <class W>
-EC_DEV void job_spec(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   const double bound = w->j_bound;
   const int incl = w->j_incl;
   const int nd = w->n_due;
@@ -1747,7 +1784,7 @@ EC_DEV void job_spec(W* w, const GP& g, int tid, int nthr) {
  * the walk to the serial fallback — writing the sorted SoA view, the
  * dependent-record flags and the horizon cut. */
 template <class W>
-EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
   const int M = w->sc.n_instances;
   for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
@@ -1812,7 +1849,7 @@ EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
       if (i < M) w->ioff[i] = (int)(run + inc - c);
       run += t_bcast_ll(inc, EC_TSIZE - 1);
     }
-    if (EC_LANE == 0) w->ioff[M] = (int)run;
+    EC_LANE0 w->ioff[M] = (int)run;
   }
   ec_team_barrier();
   for (int j = tid; j < n_all; j += nthr) {
@@ -1824,7 +1861,7 @@ EC_DEV void job_sort(W* w, const GP& g, int tid, int nthr) {
 /* JOB_APPLY (thread-level): write back every due agent's committed chain
  * prefix (records carry everything, no trace reads) and its alive slot. */
 template <class W>
-EC_DEV void job_apply(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
   const int nd = w->n_due;
   for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
@@ -1874,7 +1911,7 @@ EC_DEV void job_apply(W* w, const GP& g, int tid, int nthr) {
 
 /* JOB_INIT (thread-level): per-agent state of a fresh scenario (engine.py:251-276) */
 template <class W>
-EC_DEV void job_init(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_init(W* w, const GP& g, int tid, int nthr) {
   const int A = g.A;
   for (int a = tid; a < A; a += nthr) {
     g.ctime[a] = EC_NAN;
@@ -1914,13 +1951,13 @@ EC_DEV void job_init(W* w, const GP& g, int tid, int nthr) {
 
 /* JOB_ADMIT (warp per instance): β/γ admission of the listed instances */
 template <class W>
-EC_DEV void job_admit(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_admit(W* w, const GP& g, int tid, int nthr) {
   const int warp = tid / EC_TSIZE, nwarps = nthr >= EC_TSIZE ? nthr / EC_TSIZE : 1;
   for (int k = warp; k < w->n_eplist; k += nwarps) {
     const int i = w->ep_list[k];
     int n_start = 0;
     const int n_adm = admission(w, g, i, w->ep_gcap, &n_start);
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       w->ep_nadm[i - 1] = n_adm;
       w->ep_nstart[i - 1] = n_start;
     }
@@ -1930,7 +1967,7 @@ EC_DEV void job_admit(W* w, const GP& g, int tid, int nthr) {
 /* JOB_EPOCH (warp per instance): re-time and start admitted turns of the
  * listed instances with their precomputed push seq / start rank bases */
 template <class W>
-EC_DEV void job_epoch(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_epoch(W* w, const GP& g, int tid, int nthr) {
   const int warp = tid / EC_TSIZE, nwarps = nthr >= EC_TSIZE ? nthr / EC_TSIZE : 1;
   const double now = w->now;
   for (int k = warp; k < w->n_eplist; k += nwarps) {
@@ -1960,7 +1997,7 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
 
 /* one optimistic batch inside the current window (main warp, forks jobs) */
 template <class W, int RCAP, int DCAP, int ACAP>
-EC_DEV int batch(W* w, const GP& g, double win_end) {
+EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   /* ---- 1. due collection (shrink the window if too many agents are due) */
   EC_PROF_START(w);
   double bound = win_end;
@@ -1969,7 +2006,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   if (w->due_ready) {
     nd = w->n_cand; /* gathered by the tick sweep + epoch (may include agents no longer due) */
     t_sync();
-    if (EC_LANE == 0) w->due_ready = 0;
+    EC_LANE0 w->due_ready = 0;
   } else {
     nd = collect_due<W, DCAP>(w, g, bound, incl);
   }
@@ -1995,7 +2032,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     nd = collect_due<W, DCAP>(w, g, bound, incl);
   }
   t_sync();
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->n_due = nd;
     w->hz_t = EC_INF_BITS;
     w->hz_p = 0;
@@ -2004,7 +2041,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   t_sync();
   EC_PROF(w, 2);
   /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     int n_arr = 0;
     int p = w->arr_ptr;
     const double T = w->sc.sim_duration;
@@ -2042,7 +2079,9 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
     w->j_order_err = 0;
   }
   /* ---- 3. speculation */
+  EC_DBG(2, w->n_rec);
   fork_job(w, JOB_SPEC);
+  EC_DBG(3, w->tmp_i);
   {
     unsigned long long k = EC_INF_BITS;
     unsigned kp = 0;
@@ -2052,7 +2091,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
         kp = w->j_hz_p[q];
       }
     t_sync();
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       if (below_horizon(k, kp, -1, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
         w->hz_t = k;
         w->hz_p = (int)kp;
@@ -2069,14 +2108,17 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   fork_job(w, JOB_SORT);
+  EC_DBG(4, w->n_rec);
   const int n = w->n_rec - w->n_empty; /* empty records rank last and are never walked */
   EC_PROF(w, 3);
   /* ---- 5. commit walk: parallel segmented scans, serial fallback */
   if (!walk_parallel<W, RCAP>(w, g, n)) walk_serial(w, g, n);
+  EC_DBG(5, w->stop_kind);
   EC_PROF(w, 4);
   /* ---- 6. apply committed chain prefixes */
   fork_job(w, JOB_APPLY);
-  if (EC_LANE == 0) w->ctr[ASB_CTR_BATCHES]++;
+  EC_DBG(6, w->ctr[ASB_CTR_BATCHES]);
+  EC_LANE0 w->ctr[ASB_CTR_BATCHES]++;
   /* ---- 7. coupling / overflow follow-ups */
   const int stop = w->stop_kind;
   if (stop == STOP_COUPLING) {
@@ -2093,7 +2135,7 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
   if (stop == STOP_HORIZON) return BATCH_MORE;
   if (bound != win_end || incl != w->incl) {
     /* the shrunk window is fully committed: continue from its end */
-    if (EC_LANE == 0) w->now = bound;
+    EC_LANE0 w->now = bound;
     t_sync();
     return BATCH_MORE;
   }
@@ -2103,7 +2145,8 @@ EC_DEV int batch(W* w, const GP& g, double win_end) {
 /* exact single-event fallback: process the minimum pending event serially
  * (used only when a burst of identical timestamps exceeds the batch buffers) */
 template <class W>
-EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
+EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
+  EC_DBG(11, w->n_alive);
   unsigned long long bt = EC_INF_BITS;
   unsigned bp = 0xffffffffu;
   long long bs = 0x7fffffffffffffffll;
@@ -2140,11 +2183,12 @@ EC_DEV bool serial_step(W* w, const GP& g, double win_end) {
     double t = g.arrival[a];
     if (t < w->sc.sim_duration && key_less(ec_bits(t), EV_ARRIVAL, bt, bp)) arr = a;
   }
+  t_sync(); /* every lane has read arr_ptr before lane 0 commits an arrival */
   if (arr < 0 && ba < 0) return false;
   double t = arr >= 0 ? g.arrival[arr] : ec_from_bits(bt);
   if (!(w->incl ? t <= win_end : t < win_end)) return false;
   if (arr >= 0) {
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       w->now = t;
       commit_arrival(w, g, arr, route_arrival(w), w->arr_ptr);
     }
@@ -2176,7 +2220,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     in.key_valid = in.key_level = in.key_thr = in.key_run = 0;
     in.fifo_head = in.fifo_len = in.log_len = 0;
   }
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->now = 0.0;
     w->seq = 0;
     w->start_ctr = 0;
@@ -2191,15 +2235,34 @@ EC_DEV void run_scenario(W* w, const GP& g) {
   for (long long k = 0; k < K && w->status == 0; k++) {
     const bool last = k + 1 == K;
     const double win_end = last ? T : (double)(k + 1) * E;
-    if (EC_LANE == 0) {
+    EC_LANE0 {
       w->now = (double)k * E;
       w->incl = last ? 1 : 0;
       w->bound = win_end;
     }
     t_sync();
+    EC_DBG(0, k);
     epoch_event<W, DCAP>(w, g, k);
+    EC_DBG(1, k);
+    /* watchdog: every batch commits or executes at least one event, so a
+     * window never needs more batches than live events + arrivals (+ the
+     * window-shrink restarts); exceeding a generous bound is a bug */
+    long long guard = 64 + 4 * (long long)(g.A + w->n_alive) + 8 * (long long)g.A;
     for (;;) {
       if (w->status) break;
+      if (--guard < 0) {
+        EC_LANE0 {
+          w->status = ASB_SIMERR_LIVELOCK;
+          w->ctr[10] = k;
+          w->ctr[11] = w->stop_kind;
+          w->ctr[12] = w->n_rec;
+          w->ctr[13] = (long long)ec_bits(w->now);
+          w->ctr[14] = w->n_due;
+          w->ctr[15] = w->ctr[ASB_CTR_EVENTS];
+        }
+        t_sync();
+        break;
+      }
       int rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);
       if (rc == BATCH_MORE) continue;
       if (rc == BATCH_DONE) break;
@@ -2223,7 +2286,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     g.o_level[i] = in.level;
   }
   t_sync();
-  if (EC_LANE == 0) {
+  EC_LANE0 {
     w->ctr[ASB_CTR_STATUS] = w->status;
 #ifdef ASB_PROFILE
     for (int c = 0; c < 6; c++) w->ctr[10 + c] = w->prof[c];
