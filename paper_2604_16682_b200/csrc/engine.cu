@@ -19,7 +19,7 @@
 #define FULLMASK 0xffffffffu
 #define EC_DEV __device__ __forceinline__
 #ifndef ASB_COLD_MASK
-#define ASB_COLD_MASK 7
+#define ASB_COLD_MASK 7 /* 1 jobs, 2 serial handlers, 4 phases: out of line */
 #endif
 #define EC_COLD __device__ __noinline__
 #if ASB_COLD_MASK & 1
@@ -37,6 +37,7 @@
 #else
 #define EC_COLD3 __device__ __forceinline__
 #endif
+#define EC_COLD4 __device__ __noinline__
 #define EC_LANE ((int)(threadIdx.x & 31))
 #define EC_TSIZE 32
 #define EC_NAN __longlong_as_double(0x7ff8000000000000ll)

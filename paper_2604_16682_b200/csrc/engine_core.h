@@ -64,6 +64,9 @@
 #ifndef EC_COLD3
 #define EC_COLD3 EC_COLD /* epoch / batch phases */
 #endif
+#ifndef EC_COLD4
+#define EC_COLD4 EC_COLD /* shared helpers called from many sites */
+#endif
 
 /* EC_LANE0 { ... }: a lane-0 section of the main warp's serial code.  Lanes
  * of a warp are independently scheduled, so every lane must have read the
@@ -174,6 +177,7 @@ struct WS {
   int j_dead, j_total, j_cut, j_tie_unknown, j_order_err;
   unsigned long long j_hz_t[NW];
   unsigned j_hz_p[NW];
+  alignas(16) unsigned long long skey[2 * RCAP]; /* 16-byte sort keys (GPU counting sort) */
   unsigned long long kt[RCAP];
   long long ks[RCAP];
   unsigned char kp[RCAP];
@@ -314,7 +318,7 @@ EC_DEV void clear_event(const GP& g, int a, int inst) {
 EC_DEV void set_tp(const GP& g, int a, double tp) { g.s_tp[g.slot[a]] = tp; }
 
 template <class W>
-EC_DEV double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
+EC_COLD4 double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
   /* service_time, instance.py:184-204 */
   double base = (double)g.prefill[turn] / w->pr[level - 1] + (double)g.decode[turn] / w->dr[level - 1];
   int extra = concurrent - 1 > 0 ? concurrent - 1 : 0;
@@ -324,7 +328,7 @@ EC_DEV double svc_time(const W* w, const GP& g, long long turn, int level, int c
 }
 
 template <class W>
-EC_DEV void update_power(W* w, int i, double now) {
+EC_COLD4 void update_power(W* w, int i, double now) {
   /* _update_power, engine.py:321-327 (one lane) */
   Inst& in = w->in[i - 1];
   double wt = in.running > 0 ? w->act[in.level - 1] : w->idle[in.level - 1];
@@ -351,7 +355,7 @@ EC_DEV void sync_thrash(W* w, int i, double now) {
 /* lexicographic argmin over (usage, id), router.py:91,123,150; cand_mode:
  * 0 all instances, 1 reassignment candidates (usage > 0 or current) */
 template <class W>
-EC_DEV int argmin_usage(const W* w, int cand_mode, int current) {
+EC_COLD4 int argmin_usage(const W* w, int cand_mode, int current) {
   int best = 0;
   long long bu = 0;
   for (int i = 1; i <= w->sc.n_instances; i++) {
@@ -367,7 +371,7 @@ EC_DEV int argmin_usage(const W* w, int cand_mode, int current) {
 
 /* maybe_reassign decision once the counter reached the interval (router.py:110-128) */
 template <class W>
-EC_DEV int reassign_target(const W* w, int current) {
+EC_COLD4 int reassign_target(const W* w, int current) {
   int best = argmin_usage(w, w->sc.include_idle ? 0 : 1, current);
   if (best && best != current &&
       (double)w->in[current - 1].usage >= w->sc.imbalance_ratio * (double)w->in[best - 1].usage)
@@ -377,7 +381,7 @@ EC_DEV int reassign_target(const W* w, int current) {
 
 /* arrival routing, engine.py:496-503 / router.py:75-94,131-151 (lane 0) */
 template <class W>
-EC_DEV int route_arrival(W* w) {
+EC_COLD4 int route_arrival(W* w) {
   const AsbScenario& sc = w->sc;
   if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
     int t = (w->rr_next % sc.n_instances) + 1;
@@ -393,7 +397,7 @@ EC_DEV int route_arrival(W* w) {
 
 /* _on_arrival bookkeeping after routing (engine.py:490-507), lane 0 */
 template <class W>
-EC_DEV void commit_arrival(W* w, const GP& g, int a, int target, int order_pos) {
+EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos) {
   Inst& dst = w->in[target - 1];
   g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len, g.A)] = a;
   dst.fifo_len++;
@@ -1010,7 +1014,7 @@ EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nul
 
 /* level select + SLO boost for instance i at the epoch (controller.py:81-86,147-163) */
 template <class W>
-EC_DEV int choose_level(const W* w, int i, int* boosted) {
+EC_COLD4 int choose_level(const W* w, int i, int* boosted) {
   const AsbScenario& sc = w->sc;
   const int L = sc.n_levels;
   const long long usage = w->in[i - 1].usage;
@@ -1089,7 +1093,7 @@ EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, lon
 }
 
 template <class W>
-EC_DEV void write_decision(W* w, const GP& g, long long k, int i) {
+EC_COLD4 void write_decision(W* w, const GP& g, long long k, int i) {
   if (!g.dec_rows) return;
   const Inst& in = w->in[i - 1];
   AsbDecision& d = g.dec_rows[k * w->sc.n_instances + (i - 1)];
@@ -1783,6 +1787,133 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
  * seq only breaks exact (time, prio) ties, and an unknown seq in a tie sends
  * the walk to the serial fallback — writing the sorted SoA view, the
  * dependent-record flags and the horizon cut. */
+/* the sorted-record outputs shared by both sort implementations: the
+ * sorted SoA view at rank `rank` of record j */
+template <class W>
+EC_DEV void sort_emit(W* w, int j, int rank, unsigned long long tj, unsigned pj) {
+  const Rec& r = w->rec[j];
+  SortE& e = w->srt[rank];
+  e.tb = tj;
+  e.prio = pj;
+  e.idx = (unsigned)j;
+  w->sw_t[rank] = r.t;
+  w->sw_idx[rank] = j;
+  w->sw_prio[rank] = (unsigned char)pj;
+  w->sw_flags[rank] = (unsigned char)r.flags;
+  w->sw_inst[rank] = (short)(pj == EV_ARRIVAL ? 0 : r.inst);
+  w->sw_du[rank] = pj == EV_COMPLETE ? (long long)r.delta - ((r.flags & F_LAST) ? r.aux64 : 0) : 0;
+  w->depflag[rank] = pj == EV_ARRIVAL || (pj == EV_TOOL && (r.flags & F_CHECK));
+}
+
+#if EC_TSIZE == 32
+/* 128-bit sort key of record j: (time bits, prio, seq, index); empty
+ * records sort last.  seq -1 (unknown) sorts first inside its (t, prio)
+ * tie; such ties are flagged and resolved by the serial walk. */
+struct SKey {
+  unsigned long long k1, k2;
+};
+template <class W>
+EC_DEV SKey skey_of(const W* w, int j, int n_all) {
+  SKey k;
+  if (j >= n_all) {
+    k.k1 = ~0ull;
+    k.k2 = ~0ull;
+    return k;
+  }
+  const Rec& r = w->rec[j];
+  if (r.flags & F_EMPTY) {
+    k.k1 = ~0ull;
+    k.k2 = 0xff00000000000000ull | (unsigned long long)j;
+    return k;
+  }
+  k.k1 = ec_bits(r.t);
+  k.k2 = ((unsigned long long)(unsigned)r.prio << 56) | ((unsigned long long)(r.seq + 1) << 8) |
+         (unsigned long long)j;
+  return k;
+}
+
+/* JOB_SORT, GPU team: counting rank.  The 16-byte keys of all records are
+ * staged in shared memory; each thread ranks its records by one broadcast
+ * 128-bit load + a branch-free compare per record (independent iterations,
+ * so a lone warp keeps several loads in flight).  Keys are unique (the
+ * record index is the last component), so ranks are a permutation. */
+template <class W>
+EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
+  (void)g;
+  const int n_all = w->n_rec;
+  const int M = w->sc.n_instances;
+  const int lane = tid & 31, wid = tid >> 5;
+  ulonglong2* key = reinterpret_cast<ulonglong2*>(w->skey);
+  for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
+  for (int j = tid; j < n_all; j += nthr) {
+    const SKey k = skey_of(w, j, n_all);
+    key[j] = make_ulonglong2(k.k1, k.k2);
+  }
+  ec_team_barrier();
+  for (int j = tid; j < n_all; j += nthr) {
+    const ulonglong2 me = key[j];
+    int rank = 0;
+    int q = 0;
+#pragma unroll 1
+    for (; q + 4 <= n_all; q += 4) {
+      const ulonglong2 o0 = key[q], o1 = key[q + 1], o2 = key[q + 2], o3 = key[q + 3];
+      rank += (o0.x < me.x) | ((o0.x == me.x) & (o0.y < me.y));
+      rank += (o1.x < me.x) | ((o1.x == me.x) & (o1.y < me.y));
+      rank += (o2.x < me.x) | ((o2.x == me.x) & (o2.y < me.y));
+      rank += (o3.x < me.x) | ((o3.x == me.x) & (o3.y < me.y));
+    }
+    for (; q < n_all; q++) {
+      const ulonglong2 o = key[q];
+      rank += (o.x < me.x) | ((o.x == me.x) & (o.y < me.y));
+    }
+    const Rec& rr = w->rec[j];
+    const bool empty = rr.flags & F_EMPTY;
+    const unsigned pj = empty ? 0xffu : (unsigned)rr.prio;
+    sort_emit(w, j, rank, empty ? ~0ull : me.x, pj);
+    w->ki[rank] = (short)(empty || pj == EV_ARRIVAL ? 0 : rr.inst); /* by rank */
+    if (!empty && !below_horizon(me.x, pj, rr.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s))
+      t_atomic_min_i(&w->j_cut, rank);
+  }
+  ec_team_barrier();
+  /* exact (time, prio) ties with an unknown push seq need the serial walk */
+  int tie_unknown = 0;
+  for (int p = tid + 1; p < n_all; p += nthr) {
+    if (w->sw_prio[p] == 0xff) continue;
+    if (w->srt[p].tb == w->srt[p - 1].tb && w->sw_prio[p] == w->sw_prio[p - 1] &&
+        (w->rec[w->sw_idx[p]].seq < 0 || w->rec[w->sw_idx[p - 1]].seq < 0))
+      tie_unknown = 1;
+  }
+  if (tie_unknown) w->j_tie_unknown = 1;
+  /* per-instance lists of sorted positions, in rank order (warp 0) */
+  if (wid == 0) {
+    for (int base = 0; base < n_all; base += 32) {
+      const int p = base + lane;
+      const int ij = p < n_all ? w->ki[p] : 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, ij);
+      const int before = __popc(peers & t_lt_mask());
+      if (ij) w->krank[p] = (short)(w->icnt[ij - 1] + before); /* position in instance ij's list */
+      __syncwarp();
+      if (ij && before == 0) w->icnt[ij - 1] += __popc(peers);
+      __syncwarp();
+    }
+    long long run = 0;
+    for (int base = 0; base < M; base += 32) {
+      const int i = base + lane;
+      const long long c = i < M ? w->icnt[i] : 0;
+      const long long inc = t_scan_add_ll(c);
+      if (i < M) w->ioff[i] = (int)(run + inc - c);
+      run += t_bcast_ll(inc, 31);
+    }
+    if (lane == 0) w->ioff[M] = (int)run;
+    __syncwarp();
+    for (int p = lane; p < n_all; p += 32) {
+      const int ij = w->ki[p];
+      if (ij) w->ilist[w->ioff[ij - 1] + w->krank[p]] = (short)p;
+    }
+  }
+}
+#else
+/* JOB_SORT, generic team (the 1-lane host harness): O(n^2) rank sort */
 template <class W>
 EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
@@ -1857,6 +1988,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (ij && w->kp[j] != 0xff) w->ilist[w->ioff[ij - 1] + w->kir[j]] = w->krank[j];
   }
 }
+#endif
 
 /* JOB_APPLY (thread-level): write back every due agent's committed chain
  * prefix (records carry everything, no trace reads) and its alive slot. */
@@ -2032,6 +2164,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
     nd = collect_due<W, DCAP>(w, g, bound, incl);
   }
   t_sync();
+  EC_PROF(w, 0);
   EC_LANE0 {
     w->n_due = nd;
     w->hz_t = EC_INF_BITS;
@@ -2107,6 +2240,11 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
     t_sync();
   }
   /* ---- 4. rank sort + sorted SoA view */
+  EC_PROF(w, 2);
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK)
+  EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
+  t_sync();
+#endif
   fork_job(w, JOB_SORT);
   EC_DBG(4, w->n_rec);
   const int n = w->n_rec - w->n_empty; /* empty records rank last and are never walked */

@@ -20,7 +20,7 @@ import bench  # noqa: E402
 from paper_2604_16682_b200 import _abi  # noqa: E402
 from paper_2604_16682_b200.engine import DeviceBatch  # noqa: E402
 
-PHASES = ("tick_sweep", "epoch_instances", "due_collect", "arrivals+speculate+sort", "walk", "apply+serial")
+PHASES = ("tick_sweep+due", "epoch_instances", "arrivals+speculate", "sort", "walk", "apply+serial")
 if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
 
@@ -47,6 +47,7 @@ def main():
         "batches_per_scenario": float(ctr[:, _abi.CTR["batches"]].mean()),
         "events_per_scenario": float(ctr[:, _abi.CTR["events"]].mean()),
         "ticks_per_scenario": float(ctr[:, _abi.CTR["ticks"]].mean()),
+        "records_per_batch": None if WALK else float(ctr[:, _abi.CTR["retimes"]].sum() / ctr[:, _abi.CTR["batches"]].sum()),
     }
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 2:
