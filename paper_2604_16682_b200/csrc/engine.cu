@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(NT, 4)
     g.L = sc.n_levels;
     if (EC_LANE == 0) w->gp = g;
     __syncwarp();
-    asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
+    asb::run_scenario<W, RCAP, DCAP, ACAP>(w, w->gp); /* smem copy: no local-memory GP */
     __syncwarp();
   }
   if (EC_LANE == 0) w->job = asb::JOB_EXIT;

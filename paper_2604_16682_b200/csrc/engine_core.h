@@ -2260,8 +2260,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   /* ---- 7. coupling / overflow follow-ups */
   const int stop = w->stop_kind;
   if (stop == STOP_COUPLING) {
-    Rec r = w->stop_r;
-    exec_serial(w, g, r);
+    exec_serial(w, g, w->stop_r); /* smem record: no local-memory copy */
     EC_PROF(w, 5);
     return BATCH_MORE;
   }
