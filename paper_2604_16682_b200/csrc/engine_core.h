@@ -196,8 +196,6 @@ struct WS {
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
   unsigned long long tmin[MAXM];
-  unsigned long long part[MAXM][NTHR]; /* per-thread partial minima of the tick sweep */
-  unsigned long long wpart[MAXM][(NTHR + 31) / 32];
   /* epoch scratch (per instance) */
   long long ep_uobs[MAXM], ep_seq[MAXM];
   double ep_mintp[MAXM];
@@ -852,15 +850,11 @@ EC_DEV void helper_loop(W* w) {
 template <class W>
 EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
-  const int M = w->sc.n_instances;
   const bool tick = w->j_tick, collect = w->j_collect;
   const double bound = w->j_bound;
   const int incl = w->j_incl, token = w->j_token;
-  if (tick)
-    for (int i = 0; i < M; i++) w->part[i][tid] = EC_INF_BITS;
   const int n = w->n_alive;
-  int cur_i = 0, dead = 0;
-  unsigned long long cur_m = EC_INF_BITS;
+  int dead = 0;
   for (int base = 0; base < n; base += nthr * U) {
     double tp[U], nx[U];
     int mt[U], ag[U];
@@ -882,33 +876,17 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
         g.dstamp[ag[u]] = token;
       }
       if (!tick) continue;
-      if (ec_isnan(tp[u])) {
-        dead++;
-        continue;
-      }
-      const int ii = mt[u] & 0xff;
-      if (ii != cur_i) {
-        if (cur_i) {
-          unsigned long long& pm = w->part[cur_i - 1][tid];
-          if (cur_m < pm) pm = cur_m;
-        }
-        cur_i = ii;
-        cur_m = EC_INF_BITS;
-      }
+      /* throughputs are >= 0, so the f64 bit patterns order like the values;
+       * +inf = None (no LLM time yet) never lowers the min; the positive
+       * quiet NaN marks a finished agent (not in process) */
       const unsigned long long b = ec_bits(tp[u]);
-      if (b < cur_m) cur_m = b;
+      if (b > EC_INF_BITS)
+        dead++;
+      else if (b < EC_INF_BITS)
+        t_atomic_min_ull(&w->tmin[(mt[u] & 0xff) - 1], b);
     }
   }
-  if (!tick) return;
-  if (cur_i) {
-    unsigned long long& pm = w->part[cur_i - 1][tid];
-    if (cur_m < pm) pm = cur_m;
-  }
-  if (dead) t_atomic_add_i(&w->j_dead, dead);
-  for (int i = 0; i < M; i++) {
-    const unsigned long long v = t_warp_min_ull(w->part[i][tid]);
-    if ((tid & 31) == 0) w->wpart[i][tid >> 5] = v;
-  }
+  if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
 }
 
 /* agent-tick sweep (main warp): fork the slot sweep, fold the partial
@@ -927,15 +905,8 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
     w->j_dead = 0;
     w->j_total = 0;
   }
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS; /* the sweep's smem atomics fold into it */
   fork_job(w, JOB_SWEEP);
-  for (int i = EC_LANE; i < M; i += EC_TSIZE) {
-    unsigned long long mn = EC_INF_BITS;
-    for (int k = 0; k < W::NW; k++) {
-      const unsigned long long v = w->wpart[i][k];
-      mn = v < mn ? v : mn;
-    }
-    w->tmin[i] = mn;
-  }
   const int dead_all = w->j_dead;
   EC_LANE0 {
     w->ctr[ASB_CTR_TICKS] += n - dead_all;
