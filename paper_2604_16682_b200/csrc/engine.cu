@@ -121,7 +121,7 @@ __device__ long long* volatile g_asb_dbg;
 namespace {
 
 struct Workspace {
-  double *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue, *s_tp, *s_next;
+  double *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue, *s_tp, *s_next, *arr_t;
   long long *next_seq, *start_rank;
   int *next_prio, *sa, *logpos, *slot, *alive, *s_meta, *dstamp;
   int *ring, *log;
@@ -142,6 +142,7 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   };
   size_t na = (size_t)(total_agents > 0 ? total_agents : 1);
   Workspace t;
+  t.arr_t = (double*)take(na * 8);
   t.s_tp = (double*)take(na * 8);
   t.s_next = (double*)take(na * 8);
   t.issue = (double*)take(na * 8);
@@ -246,6 +247,7 @@ __global__ void __launch_bounds__(NT, 4)
     g.decode = tp.decode;
     g.tool = tp.tool;
     g.arr_order = tp.arrival_order + a0;
+    g.arr_t = ws.arr_t + oa;
     g.turn_base = tp.trace_turn_off[sc.trace_id];
     g.ctime = out.completion_time + oa;
     g.llm = out.llm_time + oa;

@@ -120,6 +120,13 @@ struct SortE {
   unsigned int idx;
 };
 
+/* one agent's event cursor (agent state in registers) */
+struct Cur {
+  int a, inst, phase, prio, steps, n_turns, sa;
+  double t, llm, issue, anchor, rem, done;
+  long long ctx, dec, maxctx, turn0;
+};
+
 /* per-instance engine state: InstanceState (instance.py:163-181) + _Instance (engine.py:234-247) */
 struct Inst {
   long long usage;
@@ -138,6 +145,7 @@ struct GP {
   const int* decode;
   const double* tool;
   const int* arr_order;
+  double* arr_t; /* [A] arrival times in arrival order (filled at scenario init) */
   long long turn_base;
   /* agent state (SoA, by agent) */
   double *ctime, *llm, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
@@ -206,6 +214,7 @@ struct WS {
   int n_eplist;
   double ep_gcap;
   int due[DCAP];
+  Cur ccache[DCAP]; /* due agents' state loaded by the speculation, reused by the apply */
   Rec rec[RCAP];
   SortE srt[RCAP];
   /* sorted structure-of-arrays view of the records for the commit walk */
@@ -677,11 +686,6 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
  * speculation cursor: one agent's own event chain (lane-local)
  * -------------------------------------------------------------------------- */
 
-struct Cur {
-  int a, inst, phase, prio, steps, n_turns, sa;
-  double t, llm, issue, anchor, rem, done;
-  long long ctx, dec, maxctx, turn0;
-};
 
 EC_DEV void cur_load(const GP& g, Cur& c, int a) {
   c.a = a;
@@ -1716,6 +1720,7 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   for (int d = tid; d < nd; d += nthr) {
     Cur c;
     cur_load(g, c, w->due[d]);
+    w->ccache[d] = c;
     Rec* r = &w->rec[d];
     r->seq = g.next_seq[c.a];
     if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
@@ -1968,8 +1973,7 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
   const int nd = w->n_due;
   for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
-    Cur c;
-    cur_load(g, c, w->due[d]);
+    Cur c = w->ccache[d]; /* unchanged since the speculation loaded it */
     int ri = d;
     long long nseq = -1, srank = -1;
     int lpos = -1;
@@ -2016,6 +2020,7 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
 template <class W>
 EC_COLD1 void job_init(W* w, const GP& g, int tid, int nthr) {
   const int A = g.A;
+  for (int p = tid; p < A; p += nthr) g.arr_t[p] = g.arrival[g.arr_order[p]];
   for (int a = tid; a < A; a += nthr) {
     g.ctime[a] = EC_NAN;
     g.llm[a] = 0.0;
@@ -2144,43 +2149,51 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   t_sync();
   EC_PROF(w, 2);
-  /* ---- 2. arrivals in the window (sorted by (time, trace index)) */
-  EC_LANE0 {
+  /* ---- 2. arrivals in the window (sorted by (time, trace index)): the
+   * window is a prefix of the sorted arrival times, read warp-parallel */
+  {
     int n_arr = 0;
-    int p = w->arr_ptr;
+    const int p0 = w->arr_ptr;
     const double T = w->sc.sim_duration;
-    while (p < g.A) {
-      int a = g.arr_order[p];
-      double t = g.arrival[a];
-      if (!(t < T)) break;
-      if (!(incl ? t <= bound : t < bound)) break;
-      if (n_arr == ACAP) {
-        unsigned long long tb = ec_bits(t);
+    const int nd = w->n_due;
+    for (;;) {
+      const int p = p0 + n_arr + EC_LANE;
+      const double t = p < g.A ? g.arr_t[p] : EC_INF;
+      const bool in = p < g.A && t < T && (incl ? t <= bound : t < bound);
+      const int k = ec_popc(t_ballot(in)); /* in-window lanes form a prefix */
+      const int room = ACAP - n_arr;
+      const int take = k < room ? k : room;
+      if (EC_LANE < take) {
+        Rec& r = w->rec[nd + n_arr + EC_LANE];
+        r.t = t;
+        r.prio = EV_ARRIVAL;
+        r.agent = g.arr_order[p];
+        r.seq = p; /* arrivals tie-break by trace order (engine.py:315-317) */
+        r.flags = 0;
+        r.child = -1;
+        r.inst = 0;
+      }
+      if (k > room && EC_LANE == room) {
+        /* the first arrival that does not fit bounds the batch */
+        const unsigned long long tb = ec_bits(t);
         if (below_horizon(tb, EV_ARRIVAL, p, w->hz_t, (unsigned)w->hz_p, w->hz_s)) {
           w->hz_t = tb;
           w->hz_p = EV_ARRIVAL;
           w->hz_s = p;
         }
-        break;
       }
-      Rec& r = w->rec[w->n_due + n_arr];
-      r.t = t;
-      r.prio = EV_ARRIVAL;
-      r.agent = a;
-      r.seq = p; /* arrivals tie-break by trace order (engine.py:315-317) */
-      r.flags = 0;
-      r.child = -1;
-      r.inst = 0;
-      n_arr++;
-      p++;
+      n_arr += take;
+      if (k < EC_TSIZE || take < k) break;
     }
-    w->n_arr = n_arr;
-    w->n_rec = w->n_due + n_arr;
-    w->tmp_i = 0;
-    w->n_empty = 0;
-    w->j_bound = bound;
-    w->j_incl = incl;
-    w->j_order_err = 0;
+    EC_LANE0 {
+      w->n_arr = n_arr;
+      w->n_rec = nd + n_arr;
+      w->tmp_i = 0;
+      w->n_empty = 0;
+      w->j_bound = bound;
+      w->j_incl = incl;
+      w->j_order_err = 0;
+    }
   }
   /* ---- 3. speculation */
   EC_DBG(2, w->n_rec);

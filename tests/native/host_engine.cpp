@@ -69,7 +69,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     const long long oa = out->agent_off[s], oi = out->inst_off[s];
     size_t na = (size_t)(A > 0 ? A : 1);
     asb::GP g;
-    double* f64 = (double*)calloc(na * 9, 8);
+    double* f64 = (double*)calloc(na * 10, 8);
     long long* i64 = (long long*)calloc(na * 2, 8);
     int* i32 = (int*)calloc(na * 7, 4);
     int* rl = (int*)calloc(na * (size_t)sc.n_instances * 2, 4);
@@ -83,6 +83,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.ctime = out->completion_time + oa;
     g.llm = out->llm_time + oa;
     g.s_tp = f64 + 8 * na;
+    g.arr_t = f64 + 9 * na;
     g.issue = f64 + na;
     g.anchor = f64 + 2 * na;
     g.rem = f64 + 3 * na;
