@@ -77,9 +77,21 @@ EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__doubl
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 EC_DEV long long ec_clock() { return clock64(); }
 #define EC_TID ((int)threadIdx.x)
-EC_DEV void ec_fork_begin(int nt) { asm volatile("barrier.sync 1, %0;" ::"r"(nt) : "memory"); }
-EC_DEV void ec_fork_end(int nt) { asm volatile("barrier.sync 2, %0;" ::"r"(nt) : "memory"); }
-EC_DEV void ec_team_barrier() { asm volatile("barrier.sync 3, %0;" ::"r"((int)blockDim.x) : "memory"); }
+/* named CTA barriers for the fork-join team.  Each warp reconverges first
+ * (__syncwarp): a warp that reaches a CTA barrier with some lanes still
+ * inside the job would let the barrier complete early. */
+EC_DEV void ec_fork_begin(int nt) {
+  __syncwarp();
+  asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+}
+EC_DEV void ec_fork_end(int nt) {
+  __syncwarp();
+  asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
+}
+EC_DEV void ec_team_barrier() {
+  __syncwarp();
+  asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory");
+}
 EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
 EC_DEV unsigned long long t_warp_min_ull(unsigned long long v) {
 #pragma unroll

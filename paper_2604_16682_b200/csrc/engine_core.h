@@ -87,7 +87,7 @@
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
 #endif
 #ifndef EC_SWEEP_UNROLL
-#define EC_SWEEP_UNROLL 8 /* independent loads in flight per lane in the slot sweeps */
+#define EC_SWEEP_UNROLL 4 /* independent loads in flight per lane in the slot sweeps */
 #endif
 
 namespace asb {
