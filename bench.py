@@ -10,7 +10,12 @@ simulates seeds [64r, 64r+64).  One step = every scenario of the shard run to
 completion (engine kernel + per-scenario stats + stats fold), plus the NCCL
 allreduce of the 8-double stats vector when N > 1.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config c5|c3|c4]
+
+--config selects another BASELINE.json workload for the same line format:
+c3 = the DVFS sweep (8 fixed levels x 4 capacities x 8 seeds per GPU, 1
+instance x ~1k agents, 12500 epochs), c4 = the 100k-agent thrashing regime
+(one scenario, 64 instances).  The driver's headline is the default (c5).
 
 `--impl reference` times the CPU restatement of the reference (oracle/,
 serial C DES, OpenMP over scenarios on all host cores) on the same shard.
@@ -34,7 +39,6 @@ import numpy as np  # noqa: E402
 
 METRIC = "agent-ticks/sec (batched scenarios)"
 UNIT = "agent-ticks/s"
-SEEDS_PER_GPU = 64
 HBM_FALLBACK = 6538.6
 
 
@@ -44,7 +48,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    p.add_argument("--seeds-per-gpu", type=int, default=SEEDS_PER_GPU)
+    p.add_argument("--config", choices=tuple(CONFIGS), default="c5",
+                   help="workload (BASELINE.json configs): c5 = the headline Monte-Carlo shard")
+    p.add_argument("--seeds-per-gpu", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -60,7 +66,12 @@ def dist_env():
 # ----------------------------------------------------------------------------- workload
 
 
+C3_MHZ = (660.0, 810.0, 900.0, 1035.0, 1185.0, 1350.0, 1515.0, 1680.0)
+C3_CAPS = (250_000, 500_000, 750_000, 1_000_000)
+
+
 def c5_cells():
+    """C5 cells: router {context_aware, round_robin} x controller {context_aware, off} x tau {20, 35}."""
     import paper_2604_16682_b200 as asb
 
     cells = []
@@ -73,17 +84,61 @@ def c5_cells():
     return cells
 
 
-def build_shard(rank: int, seeds_per_gpu: int):
+def c3_cells():
+    """C3 DVFS sweep cells: 8 fixed frequency levels x 4 capacities (BASELINE configs[2])."""
+    import paper_2604_16682_b200 as asb
+
+    table = asb.default_frequency_table(mhz=C3_MHZ)
+    cells = []
+    for mhz in C3_MHZ:
+        for cap in C3_CAPS:
+            cells.append(asb.SimConfig(traces=[], instance_count=1, sim_duration=12500.0,
+                                       instance=asb.InstanceConfig(capacity_tokens=cap, frequency_table=table),
+                                       controller=asb.ControllerConfig(variant="fixed", fixed_level_mhz=mhz)))
+    return cells, table
+
+
+# workload table: seeds per GPU (weak scaling: rank r takes seeds [r*k, (r+1)*k)), generator, cells
+CONFIGS = {
+    "c5": {"seeds_per_gpu": 64, "desc": "C5 Monte-Carlo sweep shard: 512 scenarios/GPU (64 seeds x 8 cells "
+                                        "{ctx-aware,round-robin} router x {ctx-aware,off} controller x tau {20,35}), "
+                                        "16 instances x ~10k agents, 3600 s",
+           "instances": 16, "epochs": 3600, "sim_duration_s": 3600.0},
+    "c3": {"seeds_per_gpu": 8, "desc": "C3 DVFS sweep shard: 256 scenarios/GPU (8 seeds x 8 fixed frequency levels "
+                                       "x 4 capacities {250k,500k,750k,1M}), 1 instance x ~1k agents, 12500 s",
+           "instances": 1, "epochs": 12500, "sim_duration_s": 12500.0},
+    "c4": {"seeds_per_gpu": 1, "desc": "C4 long-tail thrashing regime: 1 scenario/GPU, ~100k agents with "
+                                       "prefill growth 20/turn, 64 instances, context-aware without thrash avoidance, "
+                                       "3600 s",
+           "instances": 64, "epochs": 3600, "sim_duration_s": 3600.0},
+}
+
+
+def build_shard(rank: int, seeds_per_gpu: int | None = None, config: str = "c5"):
     import paper_2604_16682_b200 as asb
     from paper_2604_16682_b200 import _abi, packing
     from paper_2604_16682_b200.workload import generate_arrays
 
-    seeds = list(range(rank * seeds_per_gpu, (rank + 1) * seeds_per_gpu))
-    arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=s)) for s in seeds]
-    cells = c5_cells()
+    k = seeds_per_gpu or CONFIGS[config]["seeds_per_gpu"]
+    seeds = list(range(rank * k, (rank + 1) * k))
+    if config == "c5":
+        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=s)) for s in seeds]
+        cells, tables = c5_cells(), [asb.default_frequency_table()]
+    elif config == "c3":
+        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=0.08, duration=12500.0, seed=s)) for s in seeds]
+        cells, table = c3_cells()
+        tables = [table]
+    elif config == "c4":
+        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=100000 / 3600, duration=3600.0, seed=11 + s,
+                                                 prefill_growth_per_turn=20)) for s in seeds]
+        cells = [asb.SimConfig(traces=[], instance_count=64, sim_duration=3600.0,
+                               controller=asb.ControllerConfig(thrash_avoidance=False))]
+        tables = [asb.default_frequency_table()]
+    else:
+        raise ValueError(f"unknown config {config!r}")
     recs = [packing.scenario_record(c, t, 0) for t in range(len(seeds)) for c in cells]
     scen = np.array(recs, dtype=_abi.SCENARIO_DTYPE)
-    batch = packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables([asb.default_frequency_table()]))
+    batch = packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables(tables))
     return batch, seeds
 
 
@@ -199,7 +254,7 @@ def reference_arm(args, world, rank):
     from paper_2604_16682_b200 import _abi, _build
 
     _build.build_oracle()
-    batch, seeds = build_shard(0, args.seeds_per_gpu)
+    batch, seeds = build_shard(0, args.seeds_per_gpu, args.config)
     cores = cpu_cores()
     for _ in range(args.warmup):
         cpu_run(batch, cores)
@@ -215,24 +270,23 @@ def reference_arm(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(batch, seeds, world, "cpu"),
+        "config": config_block(batch, seeds, world, "cpu", args.config),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"one C5 shard per step: {batch.n} scenarios (seeds {seeds[0]}-{seeds[-1]} x 8 cells)"},
+                         "sample": f"one {args.config.upper()} shard per step: {batch.n} scenarios (seeds {seeds[0]}-{seeds[-1]})"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_block(batch, seeds, world, parallel):
-    from paper_2604_16682_b200 import _abi  # noqa: F401
-
+def config_block(batch, seeds, world, parallel, config="c5"):
+    cfg = CONFIGS[config]
     n_agents = batch.total_agents / max(batch.n, 1)
     tbytes = sum(getattr(batch.traces, k).nbytes for k in ("arrival", "agent_turn_off", "prefill", "decode", "tool"))
     return {
-        "workload": "C5 Monte-Carlo sweep shard: 512 scenarios/GPU (64 seeds x 8 cells {ctx-aware,round-robin} "
-                    "router x {ctx-aware,off} controller x tau {20,35}), 16 instances x ~10k agents, 3600 s",
-        "scenarios_per_gpu": batch.n, "seeds_per_gpu": len(seeds), "instances": 16,
-        "mean_agents_per_scenario": round(n_agents, 1), "sim_duration_s": 3600.0, "epochs": 3600,
+        "workload": cfg["desc"], "name": config,
+        "scenarios_per_gpu": batch.n, "seeds_per_gpu": len(seeds), "instances": cfg["instances"],
+        "mean_agents_per_scenario": round(n_agents, 1), "sim_duration_s": cfg["sim_duration_s"],
+        "epochs": cfg["epochs"],
         "parallelism": f"scenario-sharded x{world} ({parallel})",
         "l2": f"inputs larger than L2: {tbytes / 2**20:.0f} MiB trace pool + workspace per GPU, no flush",
     }
@@ -262,7 +316,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
-    batch, seeds = build_shard(rank, args.seeds_per_gpu)
+    batch, seeds = build_shard(rank, args.seeds_per_gpu, args.config)
     db = DeviceBatch(batch, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -374,7 +428,8 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (vectorised generator, reference distributions)",
-            "config": config_block(batch, seeds, world, "nccl allreduce of stats" if world > 1 else "1 GPU"),
+            "config": config_block(batch, seeds, world, "nccl allreduce of stats" if world > 1 else "1 GPU",
+                                   args.config),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "asb_engine_kernel", "kernel_ms": kern_s * 1e3,

@@ -128,6 +128,35 @@ __device__ long long* volatile g_asb_dbg;
   } while (0)
 #endif
 
+#ifndef ASB_NO_L2_HINTS
+/* the alive-slot arrays are re-read by every epoch's sweep: keep them in L2 */
+EC_DEV unsigned long long l2_keep() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+EC_DEV double ldk_f64(const double* p) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_keep()));
+  return v;
+}
+EC_DEV int ldk_i32(const int* p) {
+  int v;
+  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_keep()));
+  return v;
+}
+EC_DEV void stk_f64(double* p, double v) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(l2_keep()) : "memory");
+}
+EC_DEV void stk_i32(int* p, int v) {
+  asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(l2_keep()) : "memory");
+}
+#define EC_LDK_F64(p) ldk_f64(p)
+#define EC_LDK_I32(p) ldk_i32(p)
+#define EC_STK_F64(p, v) stk_f64((p), (v))
+#define EC_STK_I32(p, v) stk_i32((p), (v))
+#endif
+
 #include "engine_core.h"
 
 namespace {

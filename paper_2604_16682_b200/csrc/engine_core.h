@@ -83,6 +83,15 @@
   } while (0)
 #endif
 
+/* EC_LDK_* / EC_STK_*: loads / stores of the alive-slot arrays that every
+ * epoch's sweep reads, marked to stay in L2 (evict_last) on the GPU */
+#ifndef EC_LDK_F64
+#define EC_LDK_F64(p) (*(p))
+#define EC_LDK_I32(p) (*(p))
+#define EC_STK_F64(p, v) (*(p) = (v))
+#define EC_STK_I32(p, v) (*(p) = (v))
+#endif
+
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
 #endif
@@ -313,16 +322,16 @@ EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long lon
   g.next_prio[a] = prio;
   g.next_seq[a] = seq;
   const int j = g.slot[a];
-  g.s_next[j] = t;
-  g.s_meta[j] = inst | (prio << 8);
+  EC_STK_F64(&g.s_next[j], t);
+  EC_STK_I32(&g.s_meta[j], inst | (prio << 8));
 }
 
 EC_DEV void clear_event(const GP& g, int a, int inst) {
   g.next_prio[a] = 0;
-  g.s_meta[g.slot[a]] = inst;
+  EC_STK_I32(&g.s_meta[g.slot[a]], inst);
 }
 
-EC_DEV void set_tp(const GP& g, int a, double tp) { g.s_tp[g.slot[a]] = tp; }
+EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.s_tp[g.slot[a]], tp); }
 
 template <class W>
 EC_COLD4 double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
@@ -413,11 +422,11 @@ EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos
   g.phase[a] = ASB_PHASE_PENDING;
   g.next_prio[a] = 0;
   const int j = w->n_alive++;
-  g.alive[j] = a;
+  EC_STK_I32(&g.alive[j], a);
   g.slot[a] = j;
-  g.s_tp[j] = EC_INF;
-  g.s_next[j] = 0.0;
-  g.s_meta[j] = target;
+  EC_STK_F64(&g.s_tp[j], EC_INF);
+  EC_STK_F64(&g.s_next[j], 0.0);
+  EC_STK_I32(&g.s_meta[j], target);
   g.rank[a] = w->arr_rank++;
   w->arr_ptr = order_pos + 1;
   w->ctr[ASB_CTR_ARRIVED]++;
@@ -861,23 +870,23 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   int dead = 0;
   for (int base = 0; base < n; base += nthr * U) {
     double tp[U], nx[U];
-    int mt[U], ag[U];
+    int mt[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int j = base + u * nthr + tid;
       const bool ok = j < n;
-      mt[u] = ok ? g.s_meta[j] : -1;
-      tp[u] = ok && tick ? g.s_tp[j] : 0.0;
-      nx[u] = ok && collect ? g.s_next[j] : 0.0;
-      ag[u] = ok && collect ? g.alive[j] : -1;
+      mt[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
+      tp[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
+      nx[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (mt[u] < 0) continue;
       if (collect && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound)) {
+        const int a = EC_LDK_I32(&g.alive[base + u * nthr + tid]); /* only due slots need the agent id */
         const int pos = t_atomic_add_i(&w->j_total, 1);
-        if (pos < W::DC) w->due[pos] = ag[u];
-        g.dstamp[ag[u]] = token;
+        if (pos < W::DC) w->due[pos] = a;
+        g.dstamp[a] = token;
       }
       if (!tick) continue;
       /* throughputs are >= 0, so the f64 bit patterns order like the values;
@@ -936,10 +945,10 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
       t_sync();
       if (live) {
         const int o = out + ec_popc(m & t_lt_mask());
-        g.alive[o] = a;
-        g.s_tp[o] = tp;
-        g.s_next[o] = nx;
-        g.s_meta[o] = mt;
+        EC_STK_I32(&g.alive[o], a);
+        EC_STK_F64(&g.s_tp[o], tp);
+        EC_STK_F64(&g.s_next[o], nx);
+        EC_STK_I32(&g.s_meta[o], mt);
         g.slot[a] = o;
       }
       out += ec_popc(m);
@@ -959,6 +968,11 @@ EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nul
   const double now = w->now;
   long long usage = in.usage;
   int n_adm = 0, n_st = 0;
+  if (!((double)usage < gcap)) {
+    /* the head cannot be admitted (controller.py:121): nothing changes */
+    if (n_start) *n_start = 0;
+    return 0;
+  }
   for (int base = 0; base < len; base += EC_TSIZE) {
     int j = base + EC_LANE;
     bool valid = j < len;
@@ -1180,7 +1194,9 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
     int cnt = 0;
     for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
       const int i = r0 + EC_LANE + 1;
-      const bool pend = i <= M && w->in[i - 1].fifo_len > 0;
+      /* pending agents and room below gamma * cap (else admission_pass admits nothing) */
+      const bool pend = i <= M && w->in[i - 1].fifo_len > 0 &&
+                        (double)w->in[i - 1].usage < (ca ? sc.gamma : 1.0) * (double)sc.capacity;
       if (i <= M) w->ep_nstart[i - 1] = 0;
       const unsigned m = t_ballot(pend);
       if (pend) w->ep_list[cnt + ec_popc(m & t_lt_mask())] = i;
@@ -1281,8 +1297,8 @@ EC_COLD3 int count_due(const W* w, const GP& g, double bound, int incl) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
       int j = base + u * EC_TSIZE + EC_LANE;
-      mt[u] = j < n ? g.s_meta[j] : 0;
-      t[u] = j < n ? g.s_next[j] : 0.0;
+      mt[u] = j < n ? EC_LDK_I32(&g.s_meta[j]) : 0;
+      t[u] = j < n ? EC_LDK_F64(&g.s_next[j]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++)
