@@ -162,9 +162,9 @@ EC_DEV void stk_i32(int* p, int v) {
 namespace {
 
 struct Workspace {
-  double *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue, *s_tp, *s_next, *arr_t;
-  long long *next_seq, *start_rank;
-  int *next_prio, *sa, *logpos, *slot, *alive, *s_meta, *dstamp;
+  asb::AgentHot* hot;
+  double *notbefore, *pissue, *s_tp, *s_next, *arr_t;
+  int *alive, *s_meta, *dstamp;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -183,22 +183,12 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   };
   size_t na = (size_t)(total_agents > 0 ? total_agents : 1);
   Workspace t;
+  t.hot = (asb::AgentHot*)take(na * sizeof(asb::AgentHot));
   t.arr_t = (double*)take(na * 8);
   t.s_tp = (double*)take(na * 8);
   t.s_next = (double*)take(na * 8);
-  t.issue = (double*)take(na * 8);
-  t.anchor = (double*)take(na * 8);
-  t.rem = (double*)take(na * 8);
-  t.done = (double*)take(na * 8);
-  t.next_t = (double*)take(na * 8);
   t.notbefore = (double*)take(na * 8);
   t.pissue = (double*)take(na * 8);
-  t.next_seq = (long long*)take(na * 8);
-  t.start_rank = (long long*)take(na * 8);
-  t.next_prio = (int*)take(na * 4);
-  t.sa = (int*)take(na * 4);
-  t.logpos = (int*)take(na * 4);
-  t.slot = (int*)take(na * 4);
   t.alive = (int*)take(na * 4);
   t.s_meta = (int*)take(na * 4);
   t.dstamp = (int*)take(na * 4);
@@ -290,29 +280,19 @@ __global__ void __launch_bounds__(NT, 4)
     g.arr_order = tp.arrival_order + a0;
     g.arr_t = ws.arr_t + oa;
     g.turn_base = tp.trace_turn_off[sc.trace_id];
+    g.H = ws.hot + oa;
     g.ctime = out.completion_time + oa;
-    g.llm = out.llm_time + oa;
-    g.issue = ws.issue + oa;
-    g.anchor = ws.anchor + oa;
-    g.rem = ws.rem + oa;
-    g.done = ws.done + oa;
-    g.next_t = ws.next_t + oa;
     g.notbefore = ws.notbefore + oa;
     g.pissue = ws.pissue + oa;
-    g.dec = reinterpret_cast<long long*>(out.decode_total) + oa;
-    g.maxctx = reinterpret_cast<long long*>(out.max_context) + oa;
-    g.ctx = reinterpret_cast<long long*>(out.context) + oa;
-    g.next_seq = ws.next_seq + oa;
-    g.start_rank = ws.start_rank + oa;
-    g.steps = out.turns_completed + oa;
-    g.inst = out.final_instance + oa;
-    g.mig = out.migrations + oa;
-    g.phase = out.phase + oa;
     g.rank = out.arrival_rank + oa;
-    g.next_prio = ws.next_prio + oa;
-    g.sa = ws.sa + oa;
-    g.logpos = ws.logpos + oa;
-    g.slot = ws.slot + oa;
+    g.o_llm = out.llm_time + oa;
+    g.o_dec = reinterpret_cast<long long*>(out.decode_total) + oa;
+    g.o_maxctx = reinterpret_cast<long long*>(out.max_context) + oa;
+    g.o_ctx = reinterpret_cast<long long*>(out.context) + oa;
+    g.o_steps = out.turns_completed + oa;
+    g.o_inst = out.final_instance + oa;
+    g.o_mig = out.migrations + oa;
+    g.o_phase = out.phase + oa;
     g.alive = ws.alive + oa;
     g.s_tp = ws.s_tp + oa;
     g.s_next = ws.s_next + oa;

@@ -129,6 +129,16 @@ struct SortE {
   unsigned int idx;
 };
 
+/* hot per-agent state (AgentRuntimeState instance.py:148-160 + _Agent /
+ * _RunningTurn engine.py:210-231), one 128-byte record per agent so that an
+ * event touches one cache line instead of a sector in each of ~20 arrays */
+struct alignas(16) AgentHot {
+  double next_t, llm, issue, anchor, rem, done;
+  long long ctx, dec, maxctx, next_seq, start_rank;
+  int steps, inst, sa, logpos, phase, next_prio, slot, mig, pad0, pad1;
+};
+static_assert(sizeof(AgentHot) == 128, "one 128-byte line per agent");
+
 /* one agent's event cursor (agent state in registers) */
 struct Cur {
   int a, inst, phase, prio, steps, n_turns, sa;
@@ -157,9 +167,13 @@ struct GP {
   double* arr_t; /* [A] arrival times in arrival order (filled at scenario init) */
   long long turn_base;
   /* agent state (SoA, by agent) */
-  double *ctime, *llm, *issue, *anchor, *rem, *done, *next_t, *notbefore, *pissue;
-  long long *dec, *maxctx, *ctx, *next_seq, *start_rank;
-  int *steps, *inst, *mig, *phase, *rank, *next_prio, *sa, *logpos, *slot, *dstamp;
+  AgentHot* H;        /* hot per-agent state, one 128-byte record per agent */
+  double *ctime, *notbefore, *pissue;
+  int *rank, *dstamp;
+  /* outputs written from H when the scenario finishes */
+  double* o_llm;
+  long long *o_dec, *o_maxctx, *o_ctx;
+  int *o_steps, *o_inst, *o_mig, *o_phase;
   /* alive slots: the agent-tick / due sweeps read only these, coalesced */
   int* alive;      /* slot -> agent */
   double* s_tp;    /* running throughput; +inf = None; NaN = finished */
@@ -178,7 +192,7 @@ struct GP {
 };
 
 enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
-       JOB_EPOCH = 7 };
+       JOB_EPOCH = 7, JOB_FINISH = 8 };
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR>
 struct WS {
@@ -318,20 +332,20 @@ EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, uns
 
 /* next-event bookkeeping: per-agent copy + the alive-slot copy the sweeps read */
 EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long long seq) {
-  g.next_t[a] = t;
-  g.next_prio[a] = prio;
-  g.next_seq[a] = seq;
-  const int j = g.slot[a];
+  g.H[a].next_t = t;
+  g.H[a].next_prio = prio;
+  g.H[a].next_seq = seq;
+  const int j = g.H[a].slot;
   EC_STK_F64(&g.s_next[j], t);
   EC_STK_I32(&g.s_meta[j], inst | (prio << 8));
 }
 
 EC_DEV void clear_event(const GP& g, int a, int inst) {
-  g.next_prio[a] = 0;
-  EC_STK_I32(&g.s_meta[g.slot[a]], inst);
+  g.H[a].next_prio = 0;
+  EC_STK_I32(&g.s_meta[g.H[a].slot], inst);
 }
 
-EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.s_tp[g.slot[a]], tp); }
+EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.s_tp[g.H[a].slot], tp); }
 
 template <class W>
 EC_COLD4 double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
@@ -417,13 +431,13 @@ EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos
   Inst& dst = w->in[target - 1];
   g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len, g.A)] = a;
   dst.fifo_len++;
-  g.inst[a] = target;
-  g.sa[a] = 0;
-  g.phase[a] = ASB_PHASE_PENDING;
-  g.next_prio[a] = 0;
+  g.H[a].inst = target;
+  g.H[a].sa = 0;
+  g.H[a].phase = ASB_PHASE_PENDING;
+  g.H[a].next_prio = 0;
   const int j = w->n_alive++;
   EC_STK_I32(&g.alive[j], a);
-  g.slot[a] = j;
+  g.H[a].slot = j;
   EC_STK_F64(&g.s_tp[j], EC_INF);
   EC_STK_F64(&g.s_next[j], 0.0);
   EC_STK_I32(&g.s_meta[j], target);
@@ -438,7 +452,7 @@ template <class W, int DCAP>
 EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
   bool add = false;
   if (cand && a >= 0 && g.dstamp[a] != w->cand_token) {
-    const double t = g.next_t[a];
+    const double t = g.H[a].next_t;
     add = w->incl ? t <= w->bound : t < w->bound;
   }
   if (add) {
@@ -472,29 +486,29 @@ EC_COLD2 int log_pass(W* w, const GP& g, int i, int retime, long long seq0, doub
     bool live = false;
     if (p < len) {
       a = lg[p];
-      live = g.phase[a] == ASB_PHASE_RUNNING && g.inst[a] == i && g.logpos[a] == p;
+      live = g.H[a].phase == ASB_PHASE_RUNNING && g.H[a].inst == i && g.H[a].logpos == p;
     }
     unsigned m = t_ballot(live);
     int pos = out + ec_popc(m & t_lt_mask());
     t_sync(); /* every lane has read its entry before any entry is rewritten */
     if (live) {
       if (retime) {
-        double anchor = g.anchor[a], done = g.done[a], rem = g.rem[a];
+        double anchor = g.H[a].anchor, done = g.H[a].done, rem = g.H[a].rem;
         double segment = done - anchor;
         if (segment > 0) {
           double fraction_done = (now - anchor) / segment;
           double x = 1.0 - fraction_done;
           rem *= (x > 0.0 ? x : 0.0);
         }
-        long long turn = g.aturn[a] + g.steps[a];
+        long long turn = g.aturn[a] + g.H[a].steps;
         double full = svc_time(w, g, turn, level, running, thr);
         done = now + rem * full;
-        g.anchor[a] = now;
-        g.rem[a] = rem;
-        g.done[a] = done;
+        g.H[a].anchor = now;
+        g.H[a].rem = rem;
+        g.H[a].done = done;
         set_event(g, a, i, EV_COMPLETE, done, seq0 + pos);
       }
-      g.logpos[a] = pos;
+      g.H[a].logpos = pos;
       lg[pos] = a;
     }
     out += ec_popc(m);
@@ -564,16 +578,16 @@ EC_COLD2 void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
   EC_LANE0 {
     Inst& in = w->in[i - 1];
     double now = w->now;
-    long long turn = g.aturn[a] + g.steps[a];
+    long long turn = g.aturn[a] + g.H[a].steps;
     double dur = svc_time(w, g, turn, in.level, in.running, in.thr);
-    g.issue[a] = issue;
-    g.anchor[a] = now;
-    g.rem[a] = 1.0;
-    g.done[a] = now + dur;
-    g.phase[a] = ASB_PHASE_RUNNING;
+    g.H[a].issue = issue;
+    g.H[a].anchor = now;
+    g.H[a].rem = 1.0;
+    g.H[a].done = now + dur;
+    g.H[a].phase = ASB_PHASE_RUNNING;
     set_event(g, a, i, EV_COMPLETE, now + dur, w->seq++);
-    g.start_rank[a] = w->start_ctr++;
-    g.logpos[a] = log_append(w, g, i, a);
+    g.H[a].start_rank = w->start_ctr++;
+    g.H[a].logpos = log_append(w, g, i, a);
     update_power(w, i, now);
   }
   t_sync();
@@ -582,41 +596,41 @@ EC_COLD2 void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
 /* _on_complete, engine.py:509-535 */
 template <class W>
 EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
-  int i = g.inst[a];
+  int i = g.H[a].inst;
   EC_LANE0 {
     Inst& in = w->in[i - 1];
     double now = w->now;
     in.running -= 1;
-    double llm = now - g.issue[a];
-    long long turn = g.aturn[a] + g.steps[a];
+    double llm = now - g.H[a].issue;
+    long long turn = g.aturn[a] + g.H[a].steps;
     int p = g.prefill[turn], d = g.decode[turn];
-    long long ctx = g.ctx[a] + p + d;
-    int steps = g.steps[a] + 1;
-    long long dec = g.dec[a] + d;
-    double lt = g.llm[a] + llm;
-    g.ctx[a] = ctx;
-    g.steps[a] = steps;
-    g.dec[a] = dec;
-    g.llm[a] = lt;
-    if (ctx > g.maxctx[a]) g.maxctx[a] = ctx;
+    long long ctx = g.H[a].ctx + p + d;
+    int steps = g.H[a].steps + 1;
+    long long dec = g.H[a].dec + d;
+    double lt = g.H[a].llm + llm;
+    g.H[a].ctx = ctx;
+    g.H[a].steps = steps;
+    g.H[a].dec = dec;
+    g.H[a].llm = lt;
+    if (ctx > g.H[a].maxctx) g.H[a].maxctx = ctx;
     in.usage += p + d;
     w->ctr[ASB_CTR_TURNS]++;
     w->ctr[ASB_CTR_EVENTS]++;
     if (g.turn_issue) {
       long long lt_idx = turn - g.turn_base;
-      g.turn_issue[lt_idx] = g.issue[a];
+      g.turn_issue[lt_idx] = g.H[a].issue;
       g.turn_done[lt_idx] = now;
     }
     int n_turns = (int)(g.aturn[a + 1] - g.aturn[a]);
     if (steps == n_turns) {
       in.usage -= ctx;
-      g.phase[a] = ASB_PHASE_DONE;
+      g.H[a].phase = ASB_PHASE_DONE;
       g.ctime[a] = now;
       set_tp(g, a, EC_NAN);
       clear_event(g, a, i);
       w->ctr[ASB_CTR_COMPLETED]++;
     } else {
-      g.phase[a] = ASB_PHASE_TOOL;
+      g.H[a].phase = ASB_PHASE_TOOL;
       set_tp(g, a, (double)dec / lt);
       set_event(g, a, i, EV_TOOL, now + g.tool[turn], w->seq++);
     }
@@ -632,33 +646,33 @@ EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
 /* _on_tool, engine.py:537-561 */
 template <class W>
 EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
-  int source = g.inst[a];
+  int source = g.H[a].inst;
   t_sync(); /* every lane has read the source before lane 0 migrates the agent */
   EC_LANE0 {
     int target = 0;
     w->ctr[ASB_CTR_EVENTS]++;
     if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
-      int sa = g.sa[a] + 1;
+      int sa = g.H[a].sa + 1;
       if (sa >= w->sc.reassign_interval) {
         target = reassign_target(w, source);
         if (target || !w->sc.reset_only_on_reassign) sa = 0;
       }
-      g.sa[a] = sa;
+      g.H[a].sa = sa;
     }
     w->flag = target;
     if (target) {
       double now = w->now;
       Inst& src = w->in[source - 1];
       Inst& dst = w->in[target - 1];
-      g.mig[a] += 1;
+      g.H[a].mig += 1;
       w->ctr[ASB_CTR_MIGRATIONS]++;
       /* migrate_context, router.py:154-176 */
-      src.usage -= g.ctx[a];
+      src.usage -= g.H[a].ctx;
       src.thr = src.usage > w->sc.capacity;
       g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len, g.A)] = a;
       dst.fifo_len++;
-      g.inst[a] = target;
-      g.phase[a] = ASB_PHASE_PENDING;
+      g.H[a].inst = target;
+      g.H[a].phase = ASB_PHASE_PENDING;
       g.pissue[a] = now;
       g.notbefore[a] = now + w->sc.migration_delay;
       clear_event(g, a, target);
@@ -687,7 +701,7 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
   } else {
     EC_LANE0 w->ctr[ASB_CTR_EVENTS]++;
     t_sync();
-    start_turn_serial(w, g, g.inst[r.agent], r.agent, g.issue[r.agent]);
+    start_turn_serial(w, g, g.H[r.agent].inst, r.agent, g.H[r.agent].issue);
   }
 }
 
@@ -697,23 +711,24 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
 
 
 EC_DEV void cur_load(const GP& g, Cur& c, int a) {
+  const AgentHot h = g.H[a]; /* one line, 128-bit loads */
   c.a = a;
-  c.inst = g.inst[a];
-  c.phase = g.phase[a];
-  c.prio = g.next_prio[a];
-  c.t = g.next_t[a];
-  c.steps = g.steps[a];
+  c.inst = h.inst;
+  c.phase = h.phase;
+  c.prio = h.next_prio;
+  c.t = h.next_t;
+  c.steps = h.steps;
   c.turn0 = g.aturn[a];
   c.n_turns = (int)(g.aturn[a + 1] - c.turn0);
-  c.sa = g.sa[a];
-  c.llm = g.llm[a];
-  c.issue = g.issue[a];
-  c.anchor = g.anchor[a];
-  c.rem = g.rem[a];
-  c.done = g.done[a];
-  c.ctx = g.ctx[a];
-  c.dec = g.dec[a];
-  c.maxctx = g.maxctx[a];
+  c.sa = h.sa;
+  c.llm = h.llm;
+  c.issue = h.issue;
+  c.anchor = h.anchor;
+  c.rem = h.rem;
+  c.done = h.done;
+  c.ctx = h.ctx;
+  c.dec = h.dec;
+  c.maxctx = h.maxctx;
 }
 
 /* Advance the cursor over its next event, filling record r.  Mirrors the
@@ -949,7 +964,7 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
         EC_STK_F64(&g.s_tp[o], tp);
         EC_STK_F64(&g.s_next[o], nx);
         EC_STK_I32(&g.s_meta[o], mt);
-        g.slot[a] = o;
+        g.H[a].slot = o;
       }
       out += ec_popc(m);
       t_sync();
@@ -977,7 +992,7 @@ EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nul
     int j = base + EC_LANE;
     bool valid = j < len;
     int a = valid ? ring[ring_idx(head, j, g.A)] : -1;
-    long long c = valid ? g.ctx[a] : 0;
+    long long c = valid ? g.H[a].ctx : 0;
     const double nb = valid ? g.notbefore[a] : 0.0;
     long long incl = t_scan_add_ll(c);
     long long excl = incl - c;
@@ -1054,19 +1069,19 @@ EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, lon
     unsigned m = t_ballot(start);
     int sidx = started + ec_popc(m & t_lt_mask());
     if (valid) {
-      g.issue[a] = issue;
+      g.H[a].issue = issue;
       if (!start) {
-        g.phase[a] = ASB_PHASE_WAITING_START;
+        g.H[a].phase = ASB_PHASE_WAITING_START;
         set_event(g, a, i, EV_ISSUE, g.notbefore[a], seq0 + j);
       } else {
-        double dur = svc_time(w, g, g.aturn[a] + g.steps[a], lvl, 0, thr);
-        g.anchor[a] = now;
-        g.rem[a] = 1.0;
-        g.done[a] = now + dur;
-        g.phase[a] = ASB_PHASE_RUNNING;
+        double dur = svc_time(w, g, g.aturn[a] + g.H[a].steps, lvl, 0, thr);
+        g.H[a].anchor = now;
+        g.H[a].rem = 1.0;
+        g.H[a].done = now + dur;
+        g.H[a].phase = ASB_PHASE_RUNNING;
         set_event(g, a, i, EV_COMPLETE, now + dur, seq0 + j);
-        g.start_rank[a] = rank0 + sidx;
-        g.logpos[a] = log0 + sidx;
+        g.H[a].start_rank = rank0 + sidx;
+        g.H[a].logpos = log0 + sidx;
         g.log[(long long)(i - 1) * g.A + log0 + sidx] = a;
       }
     }
@@ -1137,8 +1152,8 @@ EC_COLD2 void epoch_serial(W* w, const GP& g, long long k) {
       EC_LANE0 g.pissue[a] = EC_NAN;
       if (wait) {
         EC_LANE0 {
-          g.phase[a] = ASB_PHASE_WAITING_START;
-          g.issue[a] = issue;
+          g.H[a].phase = ASB_PHASE_WAITING_START;
+          g.H[a].issue = issue;
           set_event(g, a, i, EV_ISSUE, g.notbefore[a], w->seq++);
         }
         t_sync();
@@ -1738,7 +1753,7 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
     cur_load(g, c, w->due[d]);
     w->ccache[d] = c;
     Rec* r = &w->rec[d];
-    r->seq = g.next_seq[c.a];
+    r->seq = g.H[c.a].next_seq;
     if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
       /* a candidate whose event moved out of the window (re-timed) */
       r->flags = F_EMPTY;
@@ -2004,24 +2019,24 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
       ri = r.child;
     }
     const int a = c.a;
-    g.ctx[a] = c.ctx;
-    g.dec[a] = c.dec;
-    g.maxctx[a] = c.maxctx;
-    g.llm[a] = c.llm;
-    g.steps[a] = c.steps;
-    g.sa[a] = c.sa;
-    g.phase[a] = c.phase;
-    g.issue[a] = c.issue;
-    g.anchor[a] = c.anchor;
-    g.rem[a] = c.rem;
-    g.done[a] = c.done;
+    g.H[a].ctx = c.ctx;
+    g.H[a].dec = c.dec;
+    g.H[a].maxctx = c.maxctx;
+    g.H[a].llm = c.llm;
+    g.H[a].steps = c.steps;
+    g.H[a].sa = c.sa;
+    g.H[a].phase = c.phase;
+    g.H[a].issue = c.issue;
+    g.H[a].anchor = c.anchor;
+    g.H[a].rem = c.rem;
+    g.H[a].done = c.done;
     if (c.prio > 0)
       set_event(g, a, c.inst, c.prio, c.t, nseq);
     else
       clear_event(g, a, c.inst);
     if (srank >= 0) {
-      g.start_rank[a] = srank;
-      g.logpos[a] = lpos;
+      g.H[a].start_rank = srank;
+      g.H[a].logpos = lpos;
     }
     if (c.phase == ASB_PHASE_DONE) {
       set_tp(g, a, EC_NAN);
@@ -2037,30 +2052,19 @@ template <class W>
 EC_COLD1 void job_init(W* w, const GP& g, int tid, int nthr) {
   const int A = g.A;
   for (int p = tid; p < A; p += nthr) g.arr_t[p] = g.arrival[g.arr_order[p]];
+  AgentHot h0;
+  h0.next_t = h0.llm = h0.issue = h0.anchor = h0.rem = h0.done = 0.0;
+  h0.ctx = h0.dec = h0.maxctx = h0.next_seq = 0;
+  h0.start_rank = -1;
+  h0.steps = h0.inst = h0.sa = h0.mig = h0.next_prio = h0.pad0 = h0.pad1 = 0;
+  h0.logpos = h0.slot = -1;
+  h0.phase = ASB_PHASE_ARRIVING;
   for (int a = tid; a < A; a += nthr) {
+    g.H[a] = h0;
     g.ctime[a] = EC_NAN;
-    g.llm[a] = 0.0;
-    g.issue[a] = 0.0;
-    g.anchor[a] = 0.0;
-    g.rem[a] = 0.0;
-    g.done[a] = 0.0;
-    g.next_t[a] = 0.0;
     g.notbefore[a] = 0.0;
     g.pissue[a] = EC_NAN;
-    g.dec[a] = 0;
-    g.maxctx[a] = 0;
-    g.ctx[a] = 0;
-    g.next_seq[a] = 0;
-    g.start_rank[a] = -1;
-    g.steps[a] = 0;
-    g.inst[a] = 0;
-    g.mig[a] = 0;
-    g.phase[a] = ASB_PHASE_ARRIVING;
     g.rank[a] = -1;
-    g.next_prio[a] = 0;
-    g.sa[a] = 0;
-    g.logpos[a] = -1;
-    g.slot[a] = -1;
     g.dstamp[a] = 0;
   }
   if (g.turn_issue) {
@@ -2070,6 +2074,23 @@ EC_COLD1 void job_init(W* w, const GP& g, int tid, int nthr) {
       g.turn_issue[t0 + t] = EC_NAN;
       g.turn_done[t0 + t] = EC_NAN;
     }
+  }
+}
+
+/* JOB_FINISH (thread-level): AgentResult fields from the hot records */
+template <class W>
+EC_COLD1 void job_finish(W* w, const GP& g, int tid, int nthr) {
+  (void)w;
+  for (int a = tid; a < g.A; a += nthr) {
+    const AgentHot h = g.H[a];
+    g.o_llm[a] = h.llm;
+    g.o_dec[a] = h.dec;
+    g.o_maxctx[a] = h.maxctx;
+    g.o_ctx[a] = h.ctx;
+    g.o_steps[a] = h.steps;
+    g.o_inst[a] = h.inst;
+    g.o_mig[a] = h.mig;
+    g.o_phase[a] = h.phase;
   }
 }
 
@@ -2115,6 +2136,7 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
     case JOB_APPLY: job_apply(w, g, tid, nthr); break;
     case JOB_ADMIT: job_admit(w, g, tid, nthr); break;
     case JOB_EPOCH: job_epoch(w, g, tid, nthr); break;
+    case JOB_FINISH: job_finish(w, g, tid, nthr); break;
     default: break;
   }
 }
@@ -2293,7 +2315,7 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
     if (pr <= 0) continue;
     const int a = g.alive[j];
     unsigned long long tb = ec_bits(g.s_next[j]);
-    long long s = g.next_seq[a];
+    long long s = g.H[a].next_seq;
     if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
       bt = tb;
       bp = (unsigned)pr;
@@ -2336,7 +2358,7 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   r.t = t;
   r.prio = (short)bp;
   r.agent = ba;
-  r.inst = g.inst[ba];
+  r.inst = g.H[ba].inst;
   exec_serial(w, g, r);
   return true;
 }
@@ -2422,7 +2444,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     g.o_pending[i] = in.fifo_len;
     g.o_level[i] = in.level;
   }
-  t_sync();
+  fork_job(w, JOB_FINISH);
   EC_LANE0 {
     w->ctr[ASB_CTR_STATUS] = w->status;
 #ifdef ASB_PROFILE

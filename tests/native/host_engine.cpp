@@ -70,6 +70,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     size_t na = (size_t)(A > 0 ? A : 1);
     asb::GP g;
     double* f64 = (double*)calloc(na * 10, 8);
+    asb::AgentHot* hot = (asb::AgentHot*)aligned_alloc(128, na * sizeof(asb::AgentHot));
     long long* i64 = (long long*)calloc(na * 2, 8);
     int* i32 = (int*)calloc(na * 7, 4);
     int* rl = (int*)calloc(na * (size_t)sc.n_instances * 2, 4);
@@ -80,32 +81,22 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.tool = tp->tool;
     g.arr_order = tp->arrival_order + a0;
     g.turn_base = tp->trace_turn_off[sc.trace_id];
+    g.H = hot;
     g.ctime = out->completion_time + oa;
-    g.llm = out->llm_time + oa;
     g.s_tp = f64 + 8 * na;
     g.arr_t = f64 + 9 * na;
-    g.issue = f64 + na;
-    g.anchor = f64 + 2 * na;
-    g.rem = f64 + 3 * na;
-    g.done = f64 + 4 * na;
-    g.next_t = f64 + 5 * na;
     g.notbefore = f64 + 6 * na;
     g.pissue = f64 + 7 * na;
-    g.dec = (long long*)out->decode_total + oa;
-    g.maxctx = (long long*)out->max_context + oa;
-    g.ctx = (long long*)out->context + oa;
-    g.next_seq = i64;
-    g.start_rank = i64 + na;
-    g.steps = out->turns_completed + oa;
-    g.inst = out->final_instance + oa;
-    g.mig = out->migrations + oa;
-    g.phase = out->phase + oa;
     g.rank = out->arrival_rank + oa;
-    g.next_prio = i32;
-    g.sa = i32 + na;
-    g.logpos = i32 + 2 * na;
+    g.o_llm = out->llm_time + oa;
+    g.o_dec = (long long*)out->decode_total + oa;
+    g.o_maxctx = (long long*)out->max_context + oa;
+    g.o_ctx = (long long*)out->context + oa;
+    g.o_steps = out->turns_completed + oa;
+    g.o_inst = out->final_instance + oa;
+    g.o_mig = out->migrations + oa;
+    g.o_phase = out->phase + oa;
     g.alive = i32 + 3 * na;
-    g.slot = i32 + 4 * na;
     g.s_meta = i32 + 5 * na;
     g.dstamp = i32 + 6 * na;
     g.s_next = f64;
@@ -127,6 +118,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
     err |= (int)g.o_ctr[ASB_CTR_STATUS];
     free(f64);
+    free(hot);
     free(i64);
     free(i32);
     free(rl);
