@@ -52,6 +52,8 @@ EC_DEV unsigned t_lt_mask() {
   return m;
 }
 EC_DEV int ec_popc(unsigned m) { return __popc(m); }
+EC_DEV int ec_ffs(unsigned m) { return __ffs(m); } /* 1-based lowest set bit, 0 if none */
+EC_DEV unsigned t_redux_min_u32(unsigned v) { return __reduce_min_sync(FULLMASK, v); }
 EC_DEV long long t_bcast_ll(long long v, int src) { return __shfl_sync(FULLMASK, v, src); }
 EC_DEV long long t_scan_add_ll(long long v) {
 #pragma unroll

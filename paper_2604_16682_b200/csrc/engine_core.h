@@ -1523,6 +1523,49 @@ EC_DEV void rs_store(W* w, int i, const RS& st) {
   in.energy = st.energy;
 }
 
+/* Team argmin of (usage, id) over the usage snapshot k (router.py:91,123,150):
+ * cand_mode 0 = all instances, 1 = reassignment candidates (usage > 0 or the
+ * current instance, unless include_idle).  Returns the 1-based id (0 none)
+ * and its usage in *bu.  Fast path: one warp reduction of a 32-bit
+ * (usage << 6 | id) key when every instance has a lane and usages fit. */
+template <class W>
+EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_out) {
+  const int M = w->sc.n_instances;
+  const bool all = cand_mode == 0 || w->sc.include_idle;
+  if (M <= EC_TSIZE) {
+    const int i = EC_LANE + 1;
+    const long long u = i <= M ? w->snap[k][i - 1] : 0;
+    const bool cand = i <= M && (all || u > 0 || i == cur);
+    if (!t_ballot(cand && (u < 0 || u >= (1ll << 26)))) {
+      const unsigned key = cand ? ((unsigned)u << 6) | (unsigned)(i - 1) : 0xffffffffu;
+      const unsigned mn = t_redux_min_u32(key);
+      if (mn == 0xffffffffu) return 0;
+      *bu_out = (long long)(mn >> 6);
+      return (int)(mn & 63u) + 1;
+    }
+  }
+  long long bu = 0;
+  int bi = 0;
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    const long long u = w->snap[k][i - 1];
+    if (!all && !(u > 0 || i == cur)) continue;
+    if (!bi || u < bu) {
+      bu = u;
+      bi = i;
+    }
+  }
+  for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
+    const long long ou = t_shfl_xor_ll(bu, o);
+    const int oi = t_shfl_xor_i(bi, o);
+    if (oi && (!bi || ou < bu || (ou == bu && oi < bi))) {
+      bu = ou;
+      bi = oi;
+    }
+  }
+  *bu_out = bu;
+  return bi;
+}
+
 /* Parallel commit walk (team).  The serial walk's state machine decomposes
  * by instance: usage, running count, thrash flag, power and the running log
  * of instance i change only at records on i.  Each lane owns instances and
@@ -1603,23 +1646,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     if (w->sw_prio[p] != EV_TOOL) continue;
     const int cur = w->sw_inst[p];
     long long bu = 0;
-    int bi = 0;
-    for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
-      long long u = w->snap[k][i - 1];
-      if (!sc.include_idle && !(u > 0 || i == cur)) continue;
-      if (!bi || u < bu) {
-        bu = u;
-        bi = i;
-      }
-    }
-    for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
-      long long ou = t_shfl_xor_ll(bu, o);
-      int oi = t_shfl_xor_i(bi, o);
-      if (oi && (!bi || ou < bu || (ou == bu && oi < bi))) {
-        bu = ou;
-        bi = oi;
-      }
-    }
+    const int bi = snap_argmin(w, k, 1, cur, &bu);
     if (bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu) {
       stop_p = p;
       stop_kind = STOP_COUPLING;
@@ -1688,28 +1715,18 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
       target = (w->rr_next % M) + 1;
     } else {
+      /* context_aware: lowest id below theta * cap, else argmin (router.py:85-90) */
+      int light = 0;
+      if (sc.policy == ASB_POLICY_CONTEXT_AWARE) {
+        const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+        for (int base = 0; base < M && !light; base += EC_TSIZE) {
+          const int i = base + EC_LANE + 1;
+          const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
+          if (m) light = base + ec_ffs(m);
+        }
+      }
       long long bu = 0;
-      int bi = 0, light = 0x7fffffff;
-      const double threshold = sc.consolidation_threshold * (double)sc.capacity;
-      for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
-        long long u = w->snap[k][i - 1];
-        if (sc.policy == ASB_POLICY_CONTEXT_AWARE && (double)u < threshold && i < light) light = i;
-        if (!bi || u < bu) {
-          bu = u;
-          bi = i;
-        }
-      }
-      for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
-        long long ou = t_shfl_xor_ll(bu, o);
-        int oi = t_shfl_xor_i(bi, o);
-        int ol = t_shfl_xor_i(light, o);
-        light = ol < light ? ol : light;
-        if (oi && (!bi || ou < bu || (ou == bu && oi < bi))) {
-          bu = ou;
-          bi = oi;
-        }
-      }
-      target = light != 0x7fffffff ? light : bi;
+      target = light ? light : snap_argmin(w, k, 0, 0, &bu);
     }
     EC_LANE0 {
       const Rec& r = w->rec[w->sw_idx[p]];

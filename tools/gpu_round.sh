@@ -14,3 +14,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:asb_engine -s 1 -c 1 \
     -o $OUT/engine python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $OUT/ncu_full.log 2>&1
 echo done
+# the other BASELINE configs (reported in DESIGN.md; the driver's headline is c5)
+timeout 900 python bench.py --config c3 --steps 3 --warmup 3 > $OUT/bench_c3.json 2> $OUT/bench_c3.err
+timeout 900 python bench.py --config c4 --steps 3 --warmup 3 > $OUT/bench_c4.json 2> $OUT/bench_c4.err
+echo done2
