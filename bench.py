@@ -162,11 +162,15 @@ def hbm_peak():
         return HBM_FALLBACK, "fallback (SURVEY/BASELINE measured copy bandwidth)"
 
 
-def ncu_traffic():
+def ncu_traffic(config: str):
+    """dram bytes per launch of the engine from the committed ncu capture of
+    the same workload (profiles/ncu_engine_traffic.json), else None."""
     path = os.path.join(ROOT, "profiles", "ncu_engine_traffic.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
+        if d.get("config", "c5") != config:
+            return None, None
         return d.get("dram_bytes_per_launch"), d
     except Exception:
         return None, None
@@ -369,7 +373,7 @@ def main():
     kern_s = (sum(kern_ms) / len(kern_ms)) / 1e3
     achieved = b_alg / kern_s / 1e9
     peak, peak_src = hbm_peak()
-    traffic, _ = ncu_traffic()
+    traffic, _ = ncu_traffic(args.config)
 
     # end-to-end through the public API with host buffers (pinned H2D + D2H of results)
     e2e = None

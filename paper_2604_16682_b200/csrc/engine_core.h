@@ -144,6 +144,11 @@ struct Cur {
   int a, inst, phase, prio, steps, n_turns, sa;
   double t, llm, issue, anchor, rem, done;
   long long ctx, dec, maxctx, turn0;
+  /* turn records of the current and the next turn, prefetched with the
+   * agent's state (one memory round trip for a complete -> issue chain) */
+  int pf_p0, pf_d0, pf_p1, pf_d1;
+  double pf_tool0;
+  int pf_step;
 };
 
 /* per-instance engine state: InstanceState (instance.py:163-181) + _Instance (engine.py:234-247) */
@@ -729,6 +734,40 @@ EC_DEV void cur_load(const GP& g, Cur& c, int a) {
   c.ctx = h.ctx;
   c.dec = h.dec;
   c.maxctx = h.maxctx;
+  /* the turn data the next two events read (complete: turn k; issue: k or k+1) */
+  const long long k = c.turn0 + c.steps;
+  const bool ok0 = c.steps < c.n_turns, ok1 = c.steps + 1 < c.n_turns;
+  c.pf_step = c.steps;
+  c.pf_p0 = ok0 ? g.prefill[k] : 0;
+  c.pf_d0 = ok0 ? g.decode[k] : 0;
+  c.pf_tool0 = ok0 ? g.tool[k] : 0.0;
+  c.pf_p1 = ok1 ? g.prefill[k + 1] : 0;
+  c.pf_d1 = ok1 ? g.decode[k + 1] : 0;
+}
+
+/* prefill / decode tokens of the cursor's current turn (prefetched when possible) */
+EC_DEV void cur_turn_pd(const GP& g, const Cur& c, int& p, int& d) {
+  if (c.steps == c.pf_step) {
+    p = c.pf_p0;
+    d = c.pf_d0;
+  } else if (c.steps == c.pf_step + 1) {
+    p = c.pf_p1;
+    d = c.pf_d1;
+  } else {
+    const long long turn = c.turn0 + c.steps;
+    p = g.prefill[turn];
+    d = g.decode[turn];
+  }
+}
+
+/* service_time (instance.py:184-204) from the token counts */
+template <class W>
+EC_DEV double svc_time_pd(const W* w, int p, int d, int level, int concurrent, int thr) {
+  double base = (double)p / w->pr[level - 1] + (double)d / w->dr[level - 1];
+  int extra = concurrent - 1 > 0 ? concurrent - 1 : 0;
+  double factor = 1.0 + w->sc.interference * (double)extra;
+  if (thr) factor *= w->sc.thrash_factor;
+  return base * factor;
 }
 
 /* Advance the cursor over its next event, filling record r.  Mirrors the
@@ -744,7 +783,9 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
   r.child = -1;
   if (c.prio == EV_COMPLETE) {
     long long turn = c.turn0 + c.steps;
-    int p = g.prefill[turn], d = g.decode[turn];
+    int p, d;
+    cur_turn_pd(g, c, p, d);
+    const double tool = c.steps == c.pf_step ? c.pf_tool0 : g.tool[turn];
     double llm = c.t - c.issue;
     if (apply && g.turn_issue) {
       g.turn_issue[turn - g.turn_base] = c.issue;
@@ -766,7 +807,7 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
     } else {
       c.phase = ASB_PHASE_TOOL;
       c.prio = EV_TOOL;
-      c.t = c.t + g.tool[turn];
+      c.t = c.t + tool;
       r.nt = c.t;
     }
     return true;
@@ -783,7 +824,9 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
     }
   }
   const Inst& in = w->in[c.inst - 1];
-  double dur = svc_time(w, g, c.turn0 + c.steps, in.level, in.running, in.thr);
+  int p, d;
+  cur_turn_pd(g, c, p, d);
+  double dur = svc_time_pd(w, p, d, in.level, in.running, in.thr);
   double t0 = c.t;
   c.anchor = t0;
   c.rem = 1.0;

@@ -49,6 +49,9 @@ def main():
         "ticks_per_scenario": float(ctr[:, _abi.CTR["ticks"]].mean()),
         "records_per_batch": None if WALK else float(ctr[:, _abi.CTR["retimes"]].sum() / ctr[:, _abi.CTR["batches"]].sum()),
     }
+    cells = 8 if batch.n % 8 == 0 else 1
+    res["per_cell_mean_max_Mcycles"] = [[round(float(tot[c::cells].mean()) / 1e6, 1), round(float(tot[c::cells].max()) / 1e6, 1)]
+                                        for c in range(cells)]
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 2:
         with open(sys.argv[2], "w") as fh:

@@ -88,7 +88,7 @@ def main():
         scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
         rd = float(d["dram__bytes_read.sum"][0].replace(",", "")) * scale[d["dram__bytes_read.sum"][1]]
         wr = float(d["dram__bytes_write.sum"][0].replace(",", "")) * scale[d["dram__bytes_write.sum"][1]]
-        traffic = {"tag": tag, "kernel": "asb_engine_kernel", "dram_bytes_per_launch": rd + wr,
+        traffic = {"tag": tag, "config": "c5", "kernel": "asb_engine_kernel", "dram_bytes_per_launch": rd + wr,
                    "dram_read": rd, "dram_write": wr, "source": f"profiles/{tag}/ncu_engine_full.txt"}
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_engine_traffic.json"), "w"), indent=1)
     print("wrote", dst)
