@@ -236,7 +236,7 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
 }
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
-__global__ void __launch_bounds__(NT, 4)
+__global__ void __launch_bounds__(NT, NT <= 128 ? 4 : 1)
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
@@ -376,6 +376,13 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   cudaStream_t st = (cudaStream_t)stream;
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
+  /* few large scenarios (each gets an SM of its own anyway): a 16-warp team
+   * with 4x larger optimistic batches; otherwise 4-warp teams, 4 per SM */
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool big = n_scen <= sms && total_agents >= (int64_t)n_scen * 8192;
+  if (big) return launch_engine<64, 768, 512, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16)
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   return launch_engine<64, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);

@@ -921,11 +921,11 @@ EC_DEV void helper_loop(W* w) {
 template <class W>
 EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
-  const bool tick = w->j_tick, collect = w->j_collect;
+  const bool tick = w->j_tick, collect = w->j_collect != 0, count_only = w->j_collect == 2;
   const double bound = w->j_bound;
   const int incl = w->j_incl, token = w->j_token;
   const int n = w->n_alive;
-  int dead = 0;
+  int dead = 0, counted = 0;
   for (int base = 0; base < n; base += nthr * U) {
     double tp[U], nx[U];
     int mt[U];
@@ -941,6 +941,10 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
     for (int u = 0; u < U; u++) {
       if (mt[u] < 0) continue;
       if (collect && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound)) {
+        if (count_only) {
+          counted++;
+          continue;
+        }
         const int a = EC_LDK_I32(&g.alive[base + u * nthr + tid]); /* only due slots need the agent id */
         const int pos = t_atomic_add_i(&w->j_total, 1);
         if (pos < W::DC) w->due[pos] = a;
@@ -958,6 +962,7 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
     }
   }
   if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
+  if (counted) t_atomic_add_i(&w->j_total, counted);
 }
 
 /* agent-tick sweep (main warp): fork the slot sweep, fold the partial
@@ -1343,26 +1348,20 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
  * optimistic batch
  * -------------------------------------------------------------------------- */
 
-/* count alive agents whose next event is due before `bound` (team) */
+/* count alive agents whose next event is due before `bound`: the whole
+ * team sweeps in count-only mode (main warp; forks the sweep) */
 template <class W>
-EC_COLD3 int count_due(const W* w, const GP& g, double bound, int incl) {
-  constexpr int U = EC_SWEEP_UNROLL;
-  int c = 0;
-  const int n = w->n_alive;
-  for (int base = 0; base < n; base += EC_TSIZE * U) {
-    int mt[U];
-    double t[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      int j = base + u * EC_TSIZE + EC_LANE;
-      mt[u] = j < n ? EC_LDK_I32(&g.s_meta[j]) : 0;
-      t[u] = j < n ? EC_LDK_F64(&g.s_next[j]) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++)
-      if ((mt[u] >> 8) > 0 && (incl ? t[u] <= bound : t[u] < bound)) c++;
+EC_COLD3 int count_due(W* w, const GP& g, double bound, int incl) {
+  (void)g;
+  EC_LANE0 {
+    w->j_tick = 0;
+    w->j_collect = 2;
+    w->j_bound = bound;
+    w->j_incl = incl;
+    w->j_total = 0;
   }
-  return (int)t_sum_ll(c);
+  fork_job(w, JOB_SWEEP);
+  return w->j_total;
 }
 
 /* collect due agents into w->due (up to DCAP); returns the total due count
