@@ -382,7 +382,7 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const bool big = n_scen <= sms && total_agents >= (int64_t)n_scen * 8192;
-  if (big) return launch_engine<64, 768, 512, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+  if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16)
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   return launch_engine<64, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);

@@ -93,7 +93,7 @@
 #endif
 
 #ifndef EC_DEPCAP
-#define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk */
+#define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
 #ifndef EC_SWEEP_UNROLL
 #define EC_SWEEP_UNROLL 4 /* independent loads in flight per lane in the slot sweeps */
@@ -204,6 +204,10 @@ struct WS {
   static constexpr int NT = NTHR;          /* threads of the team (main warp + helpers) */
   static constexpr int NW = (NTHR + 31) / 32;
   static constexpr int RC = RCAP, DC = DCAP, AC = ACAP;
+  /* large-batch teams: more dependent records per walk, and the apply
+   * reloads agent state instead of caching it in shared memory */
+  static constexpr int DEP = RCAP >= 512 ? 64 : EC_DEPCAP;
+  static constexpr bool CC = RCAP < 512;
   AsbScenario sc;
   GP gp;                                   /* shared with the helper warps */
   /* fork-join job state */
@@ -242,7 +246,7 @@ struct WS {
   int n_eplist;
   double ep_gcap;
   int due[DCAP];
-  Cur ccache[DCAP]; /* due agents' state loaded by the speculation, reused by the apply */
+  Cur ccache[CC ? DCAP : 1]; /* due agents' state loaded by the speculation, reused by the apply */
   Rec rec[RCAP];
   SortE srt[RCAP];
   /* sorted structure-of-arrays view of the records for the commit walk */
@@ -251,8 +255,8 @@ struct WS {
   int sw_idx[RCAP];
   short sw_inst[RCAP];
   unsigned char sw_prio[RCAP], sw_flags[RCAP];
-  int dep_pos[EC_DEPCAP];
-  long long snap[EC_DEPCAP][MAXM];
+  int dep_pos[DEP];
+  long long snap[DEP][MAXM];
   Rec stop_r;
   long long prof[6];
   long long prof_t;
@@ -1634,9 +1638,9 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     unsigned m = t_ballot(dep);
     int k = ndep + ec_popc(m & t_lt_mask());
     if (dep) {
-      if (k < EC_DEPCAP)
+      if (k < W::DEP)
         w->dep_pos[k] = p;
-      else if (k == EC_DEPCAP && p < cut)
+      else if (k == W::DEP && p < cut)
         cut = p; /* snapshot table full: stop before it */
     }
     ndep += ec_popc(m);
@@ -1645,7 +1649,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     int oc = t_shfl_xor_i(cut, o);
     cut = oc < cut ? oc : cut;
   }
-  EC_LANE0 w->n_dep = ndep < EC_DEPCAP ? ndep : EC_DEPCAP;
+  EC_LANE0 w->n_dep = ndep < W::DEP ? ndep : W::DEP;
   t_sync();
   EC_WPROF(w, 0);
   /* ---- step 1: per-instance replay up to the cut, in registers (lane
@@ -1810,7 +1814,7 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   for (int d = tid; d < nd; d += nthr) {
     Cur c;
     cur_load(g, c, w->due[d]);
-    w->ccache[d] = c;
+    if (W::CC) w->ccache[d] = c;
     Rec* r = &w->rec[d];
     r->seq = g.H[c.a].next_seq;
     if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
@@ -2063,7 +2067,11 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
   const int nd = w->n_due;
   for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
-    Cur c = w->ccache[d]; /* unchanged since the speculation loaded it */
+    Cur c; /* unchanged since the speculation loaded it */
+    if (W::CC)
+      c = w->ccache[d];
+    else
+      cur_load(g, c, w->due[d]);
     int ri = d;
     long long nseq = -1, srank = -1;
     int lpos = -1;

@@ -27,7 +27,7 @@ if WALK:
 
 def main():
     seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    batch, _ = bench.build_shard(0, seeds)
+    batch, _ = bench.build_shard(0, seeds if seeds > 0 else None, os.environ.get('ASB_CONFIG', 'c5'))
     db = DeviceBatch(batch, device="cuda:0")
     db.run()
     torch.cuda.synchronize()
@@ -43,7 +43,8 @@ def main():
         "scenarios": int(batch.n), "step_ms": e0.elapsed_time(e1),
         "mean_cycles_per_scenario": float(tot.mean()), "max_cycles_per_scenario": float(tot.max()),
         "phase_share": {p: float(prof[:, i].sum() / tot.sum()) for i, p in enumerate(PHASES)},
-        "phase_cycles_per_epoch": {p: float(prof[:, i].mean() / 3600) for i, p in enumerate(PHASES)},
+        "phase_cycles_per_epoch": {p: float(prof[:, i].mean() / float(batch.scen["n_epochs"][0]))
+                                   for i, p in enumerate(PHASES)},
         "batches_per_scenario": float(ctr[:, _abi.CTR["batches"]].mean()),
         "events_per_scenario": float(ctr[:, _abi.CTR["events"]].mean()),
         "ticks_per_scenario": float(ctr[:, _abi.CTR["ticks"]].mean()),
