@@ -71,6 +71,8 @@ EC_DEV long long t_sum_ll(long long v) {
 EC_DEV unsigned long long t_shfl_xor_ull(unsigned long long v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
 EC_DEV long long t_shfl_xor_ll(long long v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
 EC_DEV int t_shfl_xor_i(int v, int o) { return __shfl_xor_sync(FULLMASK, v, o); }
+EC_DEV long long t_shfl_up_ll(long long v, int o) { return __shfl_up_sync(FULLMASK, v, o); }
+EC_DEV int t_shfl_up_i(int v, int o) { return __shfl_up_sync(FULLMASK, v, o); }
 EC_DEV void t_atomic_min_ull(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
 EC_DEV int t_atomic_add_i(int* p, int v) { return atomicAdd(p, v); }
 EC_DEV bool ec_isnan(double x) { return isnan(x); }
@@ -330,6 +332,8 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
   using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
   static_assert(NT % 32 == 0 && NT >= 32, "team = whole warps");
+  /* 4 teams per SM need <= ~54 KB of shared memory each (228 KB per SM) */
+  static_assert(NT > 128 || MAXM > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
   const size_t smem = (sizeof(W) + 15) / 16 * 16;
   auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)

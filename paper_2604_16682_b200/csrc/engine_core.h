@@ -217,10 +217,22 @@ struct WS {
   int j_dead, j_total, j_cut, j_tie_unknown, j_order_err;
   unsigned long long j_hz_t[NW];
   unsigned j_hz_p[NW];
-  alignas(16) unsigned long long skey[2 * RCAP]; /* 16-byte sort keys (GPU counting sort) */
-  unsigned long long kt[RCAP];
-  long long ks[RCAP];
-  unsigned char kp[RCAP];
+  /* scratch reused phase by phase: the sort's keys, then the walk's scans */
+  union {
+    alignas(16) unsigned long long skey[2 * RCAP]; /* 16-byte sort keys (GPU counting sort) */
+    struct {
+      unsigned long long kt[RCAP]; /* generic (1-lane) rank sort */
+      long long ks[RCAP];
+      unsigned char kp[RCAP];
+    };
+    struct {
+      /* scan walk: per entry of the per-instance lists (ilist order) the
+       * usage, running count and log length after it, and the power-change flag */
+      long long wu[RCAP];
+      int wr[RCAP], wl[RCAP];
+      unsigned char wchg[RCAP];
+    };
+  };
   unsigned char depflag[RCAP];
   short ki[RCAP], kir[RCAP], krank[RCAP], ilist[RCAP]; /* per-instance record lists */
   int icnt[MAXM], ioff[MAXM + 1];
@@ -257,6 +269,8 @@ struct WS {
   unsigned char sw_prio[RCAP], sw_flags[RCAP];
   int dep_pos[DEP];
   long long snap[DEP][MAXM];
+  long long carry_u;
+  int carry_r, carry_l;
   Rec stop_r;
   long long prof[6];
   long long prof_t;
@@ -1479,96 +1493,6 @@ EC_COLD2 void walk_serial(W* w, const GP& g, const int n) {
   t_sync();
 }
 
-/* register state of one instance during the commit walk */
-struct RS {
-  long long usage;
-  int running, log_len;
-  double watts, t_pow, energy;
-};
-
-/* Per-instance replay of instance i's records (its sorted list) with
- * position < end, in registers: usage, running count, running log, power.
- * Stops before the first thrash flip / log overflow (position returned in
- * *flip / *lf).  If `snap`, records the usage before every dependent record.
- * Returns the position processing stopped at (end if none).  (one lane) */
-template <class W>
-EC_DEV int replay_list(W* w, const GP& g, int i, int end, bool snap, int* flip, int* lf, RS& st) {
-  const Inst& in = w->in[i - 1];
-  const long long cap = w->sc.capacity;
-  const int thr = in.thr;
-  const double act = w->act[in.level - 1], idle = w->idle[in.level - 1];
-  const int nd = snap ? w->n_dep : 0;
-  int kk = 0;
-  int dp = nd > 0 ? w->dep_pos[0] : 0x7fffffff;
-  const int k1 = w->ioff[i];
-  int stopped = end;
-  for (int k = w->ioff[i - 1]; k < k1; k++) {
-    const int p = w->ilist[k];
-    if (p >= end) break;
-    while (dp <= p) {
-      w->snap[kk][i - 1] = st.usage;
-      kk++;
-      dp = kk < nd ? w->dep_pos[kk] : 0x7fffffff;
-    }
-    if (w->sw_prio[p] == EV_COMPLETE) {
-      const long long nu = st.usage + w->sw_du[p];
-      if ((nu > cap ? 1 : 0) != thr) {
-        *flip = p;
-        stopped = p;
-        break;
-      }
-      st.usage = nu;
-      st.running -= 1;
-    } else {
-      if (st.log_len >= g.A) {
-        *lf = p;
-        stopped = p;
-        break;
-      }
-      Rec& r = w->rec[w->sw_idx[p]];
-      r.logpos = st.log_len;
-      g.log[(long long)(i - 1) * g.A + st.log_len] = r.agent;
-      st.log_len++;
-      st.running += 1;
-    }
-    const double wt = st.running > 0 ? act : idle;
-    if (wt != st.watts) {
-      const double t = w->sw_t[p];
-      st.energy += st.watts * (t - st.t_pow);
-      st.t_pow = t;
-      st.watts = wt;
-    }
-  }
-  while (dp < stopped) {
-    w->snap[kk][i - 1] = st.usage;
-    kk++;
-    dp = kk < nd ? w->dep_pos[kk] : 0x7fffffff;
-  }
-  return stopped;
-}
-
-template <class W>
-EC_DEV void rs_load(const W* w, int i, RS& st) {
-  const Inst& in = w->in[i - 1];
-  st.usage = in.usage;
-  st.running = in.running;
-  st.log_len = in.log_len;
-  st.watts = in.watts;
-  st.t_pow = in.t_pow;
-  st.energy = in.energy;
-}
-
-template <class W>
-EC_DEV void rs_store(W* w, int i, const RS& st) {
-  Inst& in = w->in[i - 1];
-  in.usage = st.usage;
-  in.running = st.running;
-  in.log_len = st.log_len;
-  in.watts = st.watts;
-  in.t_pow = st.t_pow;
-  in.energy = st.energy;
-}
-
 /* Team argmin of (usage, id) over the usage snapshot k (router.py:91,123,150):
  * cand_mode 0 = all instances, 1 = reassignment candidates (usage > 0 or the
  * current instance, unless include_idle).  Returns the 1-based id (0 none)
@@ -1652,40 +1576,84 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   EC_LANE0 w->n_dep = ndep < W::DEP ? ndep : W::DEP;
   t_sync();
   EC_WPROF(w, 0);
-  /* ---- step 1: per-instance replay up to the cut, in registers (lane
-   * i-1 owns instance i; instances 33..64 are replayed in step 3) */
-  RS st0;
-  int end0 = cut;
+  /* ---- step 1: per-instance prefix scans over the instances' record
+   * lists (ilist, grouped by instance, in walk order): usage, running count
+   * and running-log length after each record, the first thrash flip /
+   * log overflow, and the power-change points.  Segmented inclusive scans
+   * (segments = instances) across the team; values by record, in shared
+   * memory, for the snapshot and write-back lookups below. */
+  const long long cap = sc.capacity;
+  const int n_list = w->ioff[M];
   int first = cut, first_lf = cut;
-  {
-    const int i0 = EC_LANE + 1;
-    if (i0 <= M) {
-      rs_load(w, i0, st0);
-      int f = cut, l = cut;
-      end0 = replay_list(w, g, i0, cut, true, &f, &l, st0);
-      first = f;
-      first_lf = l;
+  for (int base = 0; base < n_list; base += EC_TSIZE) {
+    const int e = base + EC_LANE;
+    const bool valid = e < n_list;
+    const int p = valid ? w->ilist[e] : 0x7fffffff;
+    const int i = valid ? (int)w->sw_inst[p] : 1; /* instance of entry e */
+    const int s0 = w->ioff[i - 1];     /* first entry of its segment */
+    const bool live = valid && p < cut;
+    const int pr = live ? w->sw_prio[p] : 0;
+    const bool comp = pr == EV_COMPLETE, start = pr == EV_TOOL || pr == EV_ISSUE;
+    long long vu = comp ? w->sw_du[p] : 0;
+    int vr = comp ? -1 : (start ? 1 : 0), vl = start ? 1 : 0;
+    for (int o = 1; o < EC_TSIZE; o <<= 1) {
+      const long long nu = t_shfl_up_ll(vu, o);
+      const int nr = t_shfl_up_i(vr, o), nl = t_shfl_up_i(vl, o);
+      if (EC_LANE >= o && e - o >= s0) {
+        vu += nu;
+        vr += nr;
+        vl += nl;
+      }
     }
-    for (int i = EC_LANE + 1 + EC_TSIZE; i <= M; i += EC_TSIZE) {
-      RS t;
-      rs_load(w, i, t);
-      int f = cut, l = cut;
-      replay_list(w, g, i, cut, true, &f, &l, t);
-      first = f < first ? f : first;
-      first_lf = l < first_lf ? l : first_lf;
+    if (base > 0 && s0 < base) { /* segment continues from the previous chunk */
+      vu += w->carry_u;
+      vr += w->carry_r;
+      vl += w->carry_l;
     }
+    const Inst& in = w->in[i - 1];
+    const long long U = in.usage + vu;
+    const int R = in.running + vr, Lg = in.log_len + vl;
+    const int Rprev = R - (comp ? -1 : (start ? 1 : 0));
+    if (valid) {
+      w->wu[e] = U;
+      w->wr[e] = R;
+      w->wl[e] = Lg;
+      w->wchg[e] = (unsigned char)((R > 0) != (Rprev > 0));
+    }
+    if (live && comp && (U > cap ? 1 : 0) != in.thr && p < first) first = p;
+    if (live && start && Lg - 1 >= g.A && p < first_lf) first_lf = p;
+    t_sync();
+    if (EC_LANE == EC_TSIZE - 1) {
+      w->carry_u = vu;
+      w->carry_r = vr;
+      w->carry_l = vl;
+    }
+    t_sync();
   }
-  for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
-    int a = t_shfl_xor_i(first, o), b = t_shfl_xor_i(first_lf, o);
-    first = a < first ? a : first;
-    first_lf = b < first_lf ? b : first_lf;
-  }
-  t_sync();
+  first = (int)t_redux_min_u32((unsigned)first);
+  first_lf = (int)t_redux_min_u32((unsigned)first_lf);
   EC_WPROF(w, 1);
   /* ---- step 2: reassignment checks in order (team argmin on the snapshot) */
   int stop_p = first < first_lf ? first : first_lf;
   int stop_kind = stop_p == cut ? STOP_NONE : (first <= first_lf ? STOP_COUPLING : STOP_LOGFULL);
   const int n_dep = w->n_dep;
+  /* usage snapshots: instance i's usage just before dependent record k =
+   * its usage after its last record ahead of dep_pos[k] (binary search) */
+  for (int x = EC_LANE; x < n_dep * M; x += EC_TSIZE) {
+    const int k = x / M, i = x - k * M + 1;
+    const int dp = w->dep_pos[k];
+    if (dp >= stop_p) continue;
+    int lo = w->ioff[i - 1], hi = w->ioff[i]; /* first entry with position >= dp */
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (w->ilist[mid] < dp)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
+  }
+  t_sync();
   for (int k = 0; k < n_dep; k++) {
     const int p = w->dep_pos[k];
     if (p >= stop_p) break;
@@ -1700,24 +1668,47 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     }
   }
   EC_WPROF(w, 2);
-  /* ---- step 3: write back per-instance state (replay again if the stop
-   * lies before this lane's own replay end) */
-  {
-    const int i0 = EC_LANE + 1;
-    if (i0 <= M) {
-      if (end0 != stop_p) {
-        rs_load(w, i0, st0);
-        int f = stop_p, l = stop_p;
-        replay_list(w, g, i0, stop_p, false, &f, &l, st0);
+  /* ---- step 3: write back the committed prefix: running-log entries of
+   * the starts (parallel), then per instance the state after its last
+   * record ahead of stop_p and the power integration over its change
+   * points in order (lane per instance; engine.py:321-327) */
+  for (int e = EC_LANE; e < n_list; e += EC_TSIZE) {
+    const int p = w->ilist[e];
+    if (p >= stop_p) continue;
+    const int pr = w->sw_prio[p];
+    if (pr != EV_TOOL && pr != EV_ISSUE) continue;
+    const int i = w->sw_inst[p];
+    Rec& r = w->rec[w->sw_idx[p]];
+    r.logpos = w->wl[e] - 1;
+    g.log[(long long)(i - 1) * g.A + r.logpos] = r.agent;
+  }
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    Inst& in = w->in[i - 1];
+    const int e0 = w->ioff[i - 1], e1 = w->ioff[i];
+    int last = e0 - 1;
+    const double act = w->act[in.level - 1], idle = w->idle[in.level - 1];
+    double watts = in.watts, t_pow = in.t_pow, energy = in.energy;
+    for (int e = e0; e < e1; e++) {
+      const int p = w->ilist[e];
+      if (p >= stop_p) break;
+      last = e;
+      if (w->wchg[e] || e == e0) {
+        const double wt = w->wr[e] > 0 ? act : idle;
+        if (wt != watts) {
+          const double t = w->sw_t[p];
+          energy += watts * (t - t_pow);
+          t_pow = t;
+          watts = wt;
+        }
       }
-      rs_store(w, i0, st0);
     }
-    for (int i = EC_LANE + 1 + EC_TSIZE; i <= M; i += EC_TSIZE) {
-      RS t;
-      rs_load(w, i, t);
-      int f = stop_p, l = stop_p;
-      replay_list(w, g, i, stop_p, false, &f, &l, t);
-      rs_store(w, i, t);
+    if (last >= e0) {
+      in.usage = w->wu[last];
+      in.running = w->wr[last];
+      in.log_len = w->wl[last];
+      in.watts = watts;
+      in.t_pow = t_pow;
+      in.energy = energy;
     }
   }
   t_sync();

@@ -32,6 +32,8 @@ static inline long long t_sum_ll(long long v) { return v; }
 static inline unsigned long long t_shfl_xor_ull(unsigned long long v, int) { return v; }
 static inline long long t_shfl_xor_ll(long long v, int) { return v; }
 static inline int t_shfl_xor_i(int v, int) { return v; }
+static inline long long t_shfl_up_ll(long long v, int) { return v; }
+static inline int t_shfl_up_i(int v, int) { return v; }
 static inline void t_atomic_min_ull(unsigned long long* p, unsigned long long v) { if (v < *p) *p = v; }
 static inline int t_atomic_add_i(int* p, int v) { int o = *p; *p += v; return o; }
 static inline bool ec_isnan(double x) { return x != x; }
