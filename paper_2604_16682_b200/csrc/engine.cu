@@ -55,16 +55,25 @@ EC_DEV int ec_popc(unsigned m) { return __popc(m); }
 EC_DEV int ec_ffs(unsigned m) { return __ffs(m); } /* 1-based lowest set bit, 0 if none */
 EC_DEV unsigned t_redux_min_u32(unsigned v) { return __reduce_min_sync(FULLMASK, v); }
 EC_DEV long long t_bcast_ll(long long v, int src) { return __shfl_sync(FULLMASK, v, src); }
-EC_DEV long long t_scan_add_ll(long long v) {
-#pragma unroll
+/* warp collectives used at many call sites: out of line and rolled to keep
+ * the hot code small (the co-resident teams of an SM share the I-cache) */
+#ifndef ASB_INLINE_COLLECTIVES
+#define EC_COLL __device__ __noinline__
+#define EC_COLL_UNROLL _Pragma("unroll 1")
+#else
+#define EC_COLL EC_DEV
+#define EC_COLL_UNROLL _Pragma("unroll")
+#endif
+EC_COLL long long t_scan_add_ll(long long v) {
+EC_COLL_UNROLL
   for (int o = 1; o < 32; o <<= 1) {
     long long n = __shfl_up_sync(FULLMASK, v, o);
     if (EC_LANE >= o) v += n;
   }
   return v;
 }
-EC_DEV long long t_sum_ll(long long v) {
-#pragma unroll
+EC_COLL long long t_sum_ll(long long v) {
+EC_COLL_UNROLL
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
   return v;
 }
@@ -97,8 +106,8 @@ EC_DEV void ec_team_barrier() {
   asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory");
 }
 EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
-EC_DEV unsigned long long t_warp_min_ull(unsigned long long v) {
-#pragma unroll
+EC_COLL unsigned long long t_warp_min_ull(unsigned long long v) {
+EC_COLL_UNROLL
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long x = __shfl_xor_sync(FULLMASK, v, o);
     v = x < v ? x : v;
@@ -106,8 +115,8 @@ EC_DEV unsigned long long t_warp_min_ull(unsigned long long v) {
   return v;
 }
 /* warp min of (time bits, prio) keys */
-EC_DEV void t_warp_min_key(unsigned long long& t, unsigned& p) {
-#pragma unroll
+EC_COLL void t_warp_min_key(unsigned long long& t, unsigned& p) {
+EC_COLL_UNROLL
   for (int o = 16; o > 0; o >>= 1) {
     unsigned long long xt = __shfl_xor_sync(FULLMASK, t, o);
     unsigned xp = __shfl_xor_sync(FULLMASK, p, o);

@@ -96,7 +96,7 @@
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
 #ifndef EC_SWEEP_UNROLL
-#define EC_SWEEP_UNROLL 4 /* independent loads in flight per lane in the slot sweeps */
+#define EC_SWEEP_UNROLL 2 /* independent loads in flight per lane in the slot sweeps (small: I-cache) */
 #endif
 
 namespace asb {
@@ -279,6 +279,28 @@ struct WS {
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
  * accumulated by lane 0 and reported in counters[10..15];
  * -DASB_PROFILE -DASB_PROFILE_WALK times the commit-walk steps instead */
+#if defined(ASB_PROFILE_SWEEP)
+#define EC_SPROF_T0(w) long long sprof_t0_ = ec_clock()
+#define EC_SPROF_ADD(w, k)                                      \
+  do {                                                          \
+    if (EC_LANE == 0) (w)->prof[k] += ec_clock() - sprof_t0_;   \
+  } while (0)
+#define EC_SPROF_CNT(w, k)               \
+  do {                                   \
+    if (EC_LANE == 0) (w)->prof[k] += 1; \
+  } while (0)
+#else
+#define EC_SPROF_T0(w) \
+  do {                 \
+  } while (0)
+#define EC_SPROF_ADD(w, k) \
+  do {                     \
+  } while (0)
+#define EC_SPROF_CNT(w, k) \
+  do {                     \
+  } while (0)
+#endif
+
 #if defined(ASB_PROFILE) && defined(ASB_PROFILE_WALK)
 #define EC_WPROF_START(w) \
   do {                    \
@@ -298,7 +320,7 @@ struct WS {
 #define EC_PROF(w, k) \
   do {                \
   } while (0)
-#elif defined(ASB_PROFILE)
+#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP)
 #define EC_WPROF_START(w) \
   do {                    \
   } while (0)
@@ -944,16 +966,27 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   const int incl = w->j_incl, token = w->j_token;
   const int n = w->n_alive;
   int dead = 0, counted = 0;
+  /* software-pipelined: the next chunk's loads are in flight while this
+   * chunk is folded */
+  double tp[U], nx[U], tp2[U], nx2[U];
+  int mt[U], mt2[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int j = u * nthr + tid;
+    const bool ok = j < n;
+    mt[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
+    tp[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
+    nx[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
+  }
   for (int base = 0; base < n; base += nthr * U) {
-    double tp[U], nx[U];
-    int mt[U];
+    const int nb = base + nthr * U;
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const int j = base + u * nthr + tid;
+      const int j = nb + u * nthr + tid;
       const bool ok = j < n;
-      mt[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
-      tp[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
-      nx[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
+      mt2[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
+      tp2[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
+      nx2[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -961,12 +994,12 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       if (collect && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound)) {
         if (count_only) {
           counted++;
-          continue;
+        } else {
+          const int a = EC_LDK_I32(&g.alive[base + u * nthr + tid]); /* only due slots need the agent id */
+          const int pos = t_atomic_add_i(&w->j_total, 1);
+          if (pos < W::DC) w->due[pos] = a;
+          g.dstamp[a] = token;
         }
-        const int a = EC_LDK_I32(&g.alive[base + u * nthr + tid]); /* only due slots need the agent id */
-        const int pos = t_atomic_add_i(&w->j_total, 1);
-        if (pos < W::DC) w->due[pos] = a;
-        g.dstamp[a] = token;
       }
       if (!tick) continue;
       /* throughputs are >= 0, so the f64 bit patterns order like the values;
@@ -975,8 +1008,14 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       const unsigned long long b = ec_bits(tp[u]);
       if (b > EC_INF_BITS)
         dead++;
-      else if (b < EC_INF_BITS)
+      else if (b < w->tmin[(mt[u] & 0xff) - 1])
         t_atomic_min_ull(&w->tmin[(mt[u] & 0xff) - 1], b);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      mt[u] = mt2[u];
+      tp[u] = tp2[u];
+      nx[u] = nx2[u];
     }
   }
   if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
@@ -1000,7 +1039,9 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
     w->j_total = 0;
   }
   for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS; /* the sweep's smem atomics fold into it */
+  EC_SPROF_T0(w);
   fork_job(w, JOB_SWEEP);
+  EC_SPROF_ADD(w, 0);
   const int dead_all = w->j_dead;
   EC_LANE0 {
     w->ctr[ASB_CTR_TICKS] += n - dead_all;
@@ -2207,14 +2248,18 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   double bound = win_end;
   int incl = w->incl;
   int nd;
+  EC_SPROF_T0(w);
   if (w->due_ready) {
     nd = w->n_cand; /* gathered by the tick sweep + epoch (may include agents no longer due) */
     t_sync();
     EC_LANE0 w->due_ready = 0;
   } else {
     nd = collect_due<W, DCAP>(w, g, bound, incl);
+    EC_SPROF_ADD(w, 1);
+    EC_SPROF_CNT(w, 2);
   }
   if (nd > DCAP) {
+    EC_SPROF_CNT(w, 3);
     /* bisection: largest exclusive bound lo with count(lo) <= DCAP */
     double lo = w->now, hi = bound;
     int clo = 0;
@@ -2235,6 +2280,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
     incl = 0;
     nd = collect_due<W, DCAP>(w, g, bound, incl);
   }
+  EC_SPROF_ADD(w, 4);
   t_sync();
   EC_PROF(w, 0);
   EC_LANE0 {
@@ -2321,7 +2367,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   EC_PROF(w, 2);
-#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK)
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP)
   EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
   t_sync();
 #endif

@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 from paper_2604_16682_b200 import _build  # noqa: E402
 
 WALK = os.environ.get("ASB_PROFILE_WALK") == "1"
-os.environ["ASB_LIB"] = _build.build_cuda(profile="walk" if WALK else True)
+SWEEP = os.environ.get("ASB_PROFILE_SWEEP") == "1"
+os.environ["ASB_LIB"] = _build.build_cuda(profile="walk" if WALK else ("sweep" if SWEEP else True))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -23,6 +24,9 @@ from paper_2604_16682_b200.engine import DeviceBatch  # noqa: E402
 PHASES = ("tick_sweep+due", "epoch_instances", "arrivals+speculate", "sort", "walk", "apply+serial")
 if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
+if SWEEP:  # slots 2, 3 are event counts per epoch, not cycles
+    PHASES = ("tick_fork_cycles", "collect_due_cycles", "collect_due_calls", "bisections", "due_total_cycles", "unused")
+    WALK = True
 
 
 def main():
@@ -53,6 +57,12 @@ def main():
     cells = 8 if batch.n % 8 == 0 else 1
     res["per_cell_mean_max_Mcycles"] = [[round(float(tot[c::cells].mean()) / 1e6, 1), round(float(tot[c::cells].max()) / 1e6, 1)]
                                         for c in range(cells)]
+    if os.environ.get("ASB_DUMP_SCEN"):
+        tto = batch.traces.trace_turn_off
+        tid = batch.scen["trace_id"].astype(np.int64)
+        res["per_scenario"] = {"cycles": tot.tolist(), "turns": (tto[tid + 1] - tto[tid]).tolist(),
+                               "events": ctr[:, _abi.CTR["events"]].tolist(), "batches": ctr[:, _abi.CTR["batches"]].tolist(),
+                               "ticks": ctr[:, _abi.CTR["ticks"]].tolist()}
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 2:
         with open(sys.argv[2], "w") as fh:
