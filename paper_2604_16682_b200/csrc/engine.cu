@@ -142,7 +142,11 @@ __device__ long long* volatile g_asb_dbg;
 #endif
 
 #ifndef ASB_NO_L2_HINTS
-/* the alive-slot arrays are re-read by every epoch's sweep: keep them in L2 */
+/* the alive-slot arrays are re-read by every epoch's sweep: keep them in L2
+ * (and, with ASB_L1_KEEP, in L1) */
+#ifndef ASB_L1_KEEP
+#define ASB_L1_KEEP ""
+#endif
 EC_DEV unsigned long long l2_keep() {
   unsigned long long p;
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -150,12 +154,12 @@ EC_DEV unsigned long long l2_keep() {
 }
 EC_DEV double ldk_f64(const double* p) {
   double v;
-  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_keep()));
+  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_keep()));
   return v;
 }
 EC_DEV int ldk_i32(const int* p) {
   int v;
-  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_keep()));
+  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_keep()));
   return v;
 }
 EC_DEV void stk_f64(double* p, double v) {

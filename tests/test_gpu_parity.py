@@ -129,3 +129,30 @@ def test_c5_size_independent_properties(cuda_device):
         arrived = host["arrival_rank"][a0:a1] >= 0
         want = asb.engine.agent_ticks_closed_form(arr[arrived], comp[arrived], 1.0, int(batch.scen[s]["n_epochs"]))
         assert ctr[s, _abi.CTR["ticks"]] == want
+
+
+def test_wide_scenarios_64_instance_team(cuda_device):
+    """Scenarios with 17..64 instances run on the MAXM=64 small-team kernel."""
+    import random as _random
+
+    rng = _random.Random(5)
+    cfgs = []
+    for k in range(24):
+        spec = asb.WorkloadSpec(arrival_rate=rng.choice([0.5, 2.0]), duration=120.0, seed=100 + k)
+        d = {
+            "instances": rng.choice([17, 32, 64]),
+            "capacity": rng.choice([3000, 20_000, 100_000]),
+            "duration": 200.0,
+            "controller": {"variant": rng.choice(["context_aware", "off"]), "thrash_avoidance": rng.random() < 0.5},
+            "router": {"policy": rng.choice(["context_aware", "round_robin", "least_loaded"]),
+                       "reassign_interval": rng.choice([1, 3, 8]), "migration_delay": rng.choice([0.0, 2.0])},
+        }
+        cfgs.append(config_from_dict(asb, d, asb.generate_workload(spec)))
+    batch = prepare_batch(cfgs)
+    assert batch.max_instances > 16
+    got, gst = gpu(batch)
+    want, wst = run_oracle(batch)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
+    for f in _abi.STATS_DTYPE.names:
+        assert np.array_equal(gst[f], wst[f], equal_nan=True), f
