@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "../../include/agentsim_b200.h"
 
@@ -393,15 +395,28 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   cudaStream_t st = (cudaStream_t)stream;
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
-  /* few large scenarios (each gets an SM of its own anyway): a 16-warp team
-   * with 4x larger optimistic batches; otherwise 4-warp teams, 4 per SM */
+  /* team shape by scenario size (ASB_TEAM=solo|quad|big overrides, for tests):
+   *  - few large scenarios (each gets an SM of its own anyway): a 16-warp
+   *    team with 5x larger optimistic batches;
+   *  - small scenarios (< 2k agents on average): a single warp, no fork-join
+   *    barriers (their per-epoch work is a few events);
+   *  - otherwise 4-warp teams, 4 per SM. */
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool big = n_scen <= sms && total_agents >= (int64_t)n_scen * 8192;
+  const int64_t per = n_scen > 0 ? total_agents / n_scen : 0;
+  bool big = n_scen <= sms && per >= 8192;
+  bool solo = !big && per < 2048;
+  if (const char* force = getenv("ASB_TEAM")) {
+    big = !strcmp(force, "big");
+    solo = !strcmp(force, "solo");
+  }
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
-  if (max_instances <= 16)
+  if (max_instances <= 16) {
+    if (solo) return launch_engine<16, 192, 128, 64, 32>(d_scen, n_scen, traces, tables, out, ws, st);
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
+  }
+  if (solo) return launch_engine<64, 192, 128, 64, 32>(d_scen, n_scen, traces, tables, out, ws, st);
   return launch_engine<64, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
 }
 

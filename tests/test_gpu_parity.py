@@ -65,8 +65,18 @@ def _random_configs(seed, n):
     return random_configs(seed, n)
 
 
-@pytest.mark.parametrize("seed", [11, 12, 13])
-def test_random_batch_matches_oracle(cuda_device, seed):
+@pytest.fixture
+def team(request, monkeypatch):
+    """Force the engine's team shape (ASB_TEAM, read by asb_run_scenarios)."""
+    if request.param:
+        monkeypatch.setenv("ASB_TEAM", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("seed,team", [(11, None), (12, "quad"), (13, "big"), (14, "solo")], indirect=["team"])
+def test_random_batch_matches_oracle(cuda_device, seed, team):
+    """Random configurations on every team shape: solo warp (the default for
+    these small scenarios), 4-warp quad team, 16-warp big team."""
     batch = prepare_batch(_random_configs(seed, 96))
     got, gst = gpu(batch)
     want, wst = run_oracle(batch)
