@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200.so")
 PROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_prof.so")
 WPROF_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_wprof.so")
 DEBUG_LIB_PATH = os.path.join(LIB_DIR, "libagentsim_b200_debug.so")
+TRACE_IO_LIB = os.path.join(LIB_DIR, "libagentsim_trace_io.so")
 ORACLE_LIB = os.path.join(ROOT, "oracle", "build", "liboracle.so")
 HOST_ENGINE_LIB = os.path.join(ROOT, "tests", "native", "build", "libhost_engine.so")
 
@@ -76,6 +77,16 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
     return target
 
 
+def build_trace_io(force: bool = False) -> str:
+    """Host-side native JSON-lines trace reader (csrc/trace_io.cpp)."""
+    src = os.path.join(CSRC, "trace_io.cpp")
+    if force or _stale(TRACE_IO_LIB, [src]):
+        os.makedirs(LIB_DIR, exist_ok=True)
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", TRACE_IO_LIB + ".tmp", src])
+        os.replace(TRACE_IO_LIB + ".tmp", TRACE_IO_LIB)
+    return TRACE_IO_LIB
+
+
 def build_oracle(force: bool = False) -> str:
     src = os.path.join(ROOT, "oracle", "des_oracle.c")
     deps = [src, os.path.join(ROOT, "include", "agentsim_b200.h")]
@@ -100,6 +111,7 @@ def build_host_engine(force: bool = False) -> str:
 
 def build_all(force: bool = False) -> None:
     build_cuda(force)
+    build_trace_io(force)
     build_cuda(force, profile=True)
     build_cuda(force, profile="walk")
     build_oracle(force)

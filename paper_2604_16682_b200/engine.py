@@ -26,7 +26,7 @@ from .errors import ConfigurationError, SimulationError
 from .instance import InstanceConfig
 from .metrics import AgentMetrics, SystemMetrics
 from .router import RouterConfig
-from .workload import AgentTrace, WorkloadSpec, generate_workload, load_trace
+from .workload import AgentTrace, WorkloadSpec, generate_workload, load_trace, load_trace_arrays
 
 
 @dataclass
@@ -259,7 +259,14 @@ def prepare_batch(configs: Sequence[SimConfig]) -> packing.Batch:
         key = _trace_key(c)
         if key not in trace_index:
             trace_index[key] = len(trace_arrays)
-            trace_arrays.append(packing.trace_arrays_from_objects(_resolve(c, key)))
+            if key[0] == "path":
+                arrs = load_trace_arrays(c.trace_path)  # native JSONL -> CSR (csrc/trace_io.cpp)
+                ids = arrs["agent_ids"]
+                if len(set(ids)) != len(ids):  # the reference's duplicate check and message
+                    _resolve(c, key)
+            else:
+                arrs = packing.trace_arrays_from_objects(_resolve(c, key))
+            trace_arrays.append(arrs)
         tab = c.instance.frequency_table
         if tab not in table_index:
             table_index[tab] = len(tables)

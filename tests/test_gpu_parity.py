@@ -166,3 +166,22 @@ def test_wide_scenarios_64_instance_team(cuda_device):
     assert diff is None, diff
     for f in _abi.STATS_DTYPE.names:
         assert np.array_equal(gst[f], wst[f], equal_nan=True), f
+
+
+def test_run_sharded_single_rank(cuda_device):
+    """parallel.run_sharded on one rank: the LPT shard is everything, the
+    gathered per-scenario rows and the stats vector match the oracle."""
+    from paper_2604_16682_b200.parallel import run_sharded
+
+    cfgs = _random_configs(21, 12)
+    res = run_sharded(cfgs, device="cuda:0", results=True)
+    assert res.world == 1 and list(res.local_index) == list(range(len(cfgs)))
+    batch = prepare_batch(cfgs)
+    want, wst = run_oracle(batch, decisions=False, turn_log=False)
+    ctr = want["counters"].reshape(-1, _abi.ASB_NCOUNTERS)
+    assert np.array_equal(res.counters[:, :9], ctr[:, :9])
+    for f in _abi.STATS_DTYPE.names:
+        assert np.array_equal(res.stats[f], wst[f], equal_nan=True), f
+    assert res.totals["ticks"] == float(ctr[:, _abi.CTR["ticks"]].sum())
+    assert res.totals["completed"] == float(ctr[:, _abi.CTR["completed"]].sum())
+    assert len(res.local_results) == len(cfgs)
