@@ -230,7 +230,6 @@ struct WS {
        * usage, running count and log length after it, and the power-change flag */
       long long wu[RCAP];
       int wr[RCAP], wl[RCAP];
-      unsigned char wchg[RCAP];
     };
   };
   unsigned char depflag[RCAP];
@@ -271,6 +270,7 @@ struct WS {
   long long snap[DEP][MAXM];
   long long carry_u;
   int carry_r, carry_l;
+  unsigned wmask[(RCAP + 31) / 32]; /* power-change entries of the scan walk, one bit per ilist entry */
   Rec stop_r;
   long long prof[6];
   long long prof_t;
@@ -1655,11 +1655,21 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     const long long U = in.usage + vu;
     const int R = in.running + vr, Lg = in.log_len + vl;
     const int Rprev = R - (comp ? -1 : (start ? 1 : 0));
+    const bool chg = valid && ((R > 0) != (Rprev > 0) || e == s0); /* a segment's first entry always checks */
     if (valid) {
       w->wu[e] = U;
       w->wr[e] = R;
       w->wl[e] = Lg;
-      w->wchg[e] = (unsigned char)((R > 0) != (Rprev > 0));
+    }
+    {
+      const unsigned cm = t_ballot(chg);
+      if (EC_TSIZE == 32) {
+        if (EC_LANE == 0) w->wmask[base >> 5] = cm;
+      } else if (EC_LANE == 0) { /* 1-lane host build: one bit per entry */
+        unsigned& m = w->wmask[e >> 5];
+        if ((e & 31) == 0) m = 0;
+        if (chg) m |= 1u << (e & 31);
+      }
     }
     if (live && comp && (U > cap ? 1 : 0) != in.thr && p < first) first = p;
     if (live && start && Lg - 1 >= g.A && p < first_lf) first_lf = p;
@@ -1725,23 +1735,36 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   }
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     Inst& in = w->in[i - 1];
-    const int e0 = w->ioff[i - 1], e1 = w->ioff[i];
-    int last = e0 - 1;
+    const int e0 = w->ioff[i - 1];
+    int lo = e0, hi = w->ioff[i]; /* entries [e0, lo) lie before stop_p */
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (w->ilist[mid] < stop_p)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    const int last = lo - 1;
     const double act = w->act[in.level - 1], idle = w->idle[in.level - 1];
     double watts = in.watts, t_pow = in.t_pow, energy = in.energy;
-    for (int e = e0; e < e1; e++) {
-      const int p = w->ilist[e];
-      if (p >= stop_p) break;
-      last = e;
-      if (w->wchg[e] || e == e0) {
-        const double wt = w->wr[e] > 0 ? act : idle;
-        if (wt != watts) {
-          const double t = w->sw_t[p];
-          energy += watts * (t - t_pow);
-          t_pow = t;
-          watts = wt;
-        }
+    /* power changes only where the running count crosses zero: visit those
+     * entries (bitmask), in order */
+    for (int e = e0; e <= last;) {
+      const unsigned m = w->wmask[e >> 5] >> (e & 31);
+      if (!m) {
+        e = (e | 31) + 1;
+        continue;
       }
+      e += ec_ffs(m) - 1;
+      if (e > last) break;
+      const double wt = w->wr[e] > 0 ? act : idle;
+      if (wt != watts) {
+        const double t = w->sw_t[w->ilist[e]];
+        energy += watts * (t - t_pow);
+        t_pow = t;
+        watts = wt;
+      }
+      e++;
     }
     if (last >= e0) {
       in.usage = w->wu[last];

@@ -1,3 +1,6 @@
+for v in _prev "" _prev ""; do
+  L=paper_2604_16682_b200/_lib/libagentsim_b200$v.so
+  r=$(ASB_LIB=$L timeout 300 python bench.py --steps 5 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.1f'%d['ms_per_step'])" 2>&1 | tail -1)
+  echo "lib$v: $r ms"
+done
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-timeout 600 python bench.py --config c3 --steps 3 --warmup 2 --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c3', d['ms_per_step'], '%.3g'%d['value'], d['parity'], 'cpu %.3g'%d['cpu_baseline']['value'])"
-timeout 600 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c5', d['ms_per_step'])"
