@@ -1329,7 +1329,10 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
       w->ep_gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
     }
     t_sync();
-    if (cnt) fork_job(w, JOB_ADMIT);
+    if (cnt) {
+      EC_SPROF_CNT(w, 5);
+      fork_job(w, JOB_ADMIT);
+    }
   }
   /* (c) lane per instance: deferral, thrash sync, rate key, push counts;
    * exclusive scans over instances -> each instance's first push seq and
@@ -1392,7 +1395,10 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   t_sync();
   /* (d)+(e) re-time in-flight turns where the rate key changed, then start
    * the admitted turns — instances in parallel, one warp each (JOB_EPOCH) */
-  if (nwork) fork_job(w, JOB_EPOCH);
+  if (nwork) {
+    EC_SPROF_CNT(w, 2);
+    fork_job(w, JOB_EPOCH);
+  }
   /* (f) lane per instance: final power, decision rows */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     update_power(w, i, now);
@@ -2279,7 +2285,6 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   } else {
     nd = collect_due<W, DCAP>(w, g, bound, incl);
     EC_SPROF_ADD(w, 1);
-    EC_SPROF_CNT(w, 2);
   }
   if (nd > DCAP) {
     EC_SPROF_CNT(w, 3);

@@ -25,7 +25,8 @@ PHASES = ("tick_sweep+due", "epoch_instances", "arrivals+speculate", "sort", "wa
 if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
 if SWEEP:  # slots 2, 3 are event counts per epoch, not cycles
-    PHASES = ("tick_fork_cycles", "collect_due_cycles", "collect_due_calls", "bisections", "due_total_cycles", "unused")
+    PHASES = ("tick_fork_cycles", "collect_due_cycles", "epoch_job_forks", "bisections", "due_total_cycles",
+              "admit_job_forks")
     WALK = True
 
 
