@@ -1540,6 +1540,48 @@ EC_COLD2 void walk_serial(W* w, const GP& g, const int n) {
   t_sync();
 }
 
+/* usage snapshots for many instances (M > team width): lane per instance,
+ * merging its sorted record list with the sorted dependent positions */
+template <class W>
+EC_COLD4 void snapshots_merge(W* w, int n_dep, int stop_p) {
+  const int M = w->sc.n_instances;
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    const int e1 = w->ioff[i];
+    int e = w->ioff[i - 1];
+    long long u = w->in[i - 1].usage;
+    for (int k = 0; k < n_dep; k++) {
+      const int dp = w->dep_pos[k];
+      if (dp >= stop_p) break;
+      while (e < e1 && w->ilist[e] < dp) {
+        u = w->wu[e];
+        e++;
+      }
+      w->snap[k][i - 1] = u;
+    }
+  }
+}
+
+/* snap_argmin for M up to 64: each lane folds its instances into one 32-bit
+ * key, one warp reduction; -1 when a usage does not fit the key */
+template <class W>
+EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* bu_out) {
+  const int M = w->sc.n_instances;
+  unsigned key = 0xffffffffu;
+  bool wide = false;
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    const long long u = w->snap[k][i - 1];
+    if (!(all || u > 0 || i == cur)) continue;
+    wide |= u < 0 || u >= (1ll << 26);
+    const unsigned kk = ((unsigned)u << 6) | (unsigned)(i - 1);
+    key = kk < key ? kk : key;
+  }
+  if (t_ballot(wide)) return -1;
+  const unsigned mn = t_redux_min_u32(key);
+  if (mn == 0xffffffffu) return 0;
+  *bu_out = (long long)(mn >> 6);
+  return (int)(mn & 63u) + 1;
+}
+
 /* Team argmin of (usage, id) over the usage snapshot k (router.py:91,123,150):
  * cand_mode 0 = all instances, 1 = reassignment candidates (usage > 0 or the
  * current instance, unless include_idle).  Returns the 1-based id (0 none)
@@ -1560,6 +1602,9 @@ EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_
       *bu_out = (long long)(mn >> 6);
       return (int)(mn & 63u) + 1;
     }
+  } else {
+    const int r = snap_argmin_wide(w, k, all, cur, bu_out);
+    if (r >= 0) return r;
   }
   long long bu = 0;
   int bi = 0;
@@ -1695,20 +1740,27 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   int stop_kind = stop_p == cut ? STOP_NONE : (first <= first_lf ? STOP_COUPLING : STOP_LOGFULL);
   const int n_dep = w->n_dep;
   /* usage snapshots: instance i's usage just before dependent record k =
-   * its usage after its last record ahead of dep_pos[k] (binary search) */
-  for (int x = EC_LANE; x < n_dep * M; x += EC_TSIZE) {
-    const int k = x / M, i = x - k * M + 1;
-    const int dp = w->dep_pos[k];
-    if (dp >= stop_p) continue;
-    int lo = w->ioff[i - 1], hi = w->ioff[i]; /* first entry with position >= dp */
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (w->ilist[mid] < dp)
-        lo = mid + 1;
-      else
-        hi = mid;
+   * its usage after its last record ahead of dep_pos[k].  Few instances:
+   * one binary search per (record, instance) pair across the lanes; many
+   * instances (M > 32): lane per instance, merging its sorted record list
+   * with the sorted dependent positions */
+  if (M <= EC_TSIZE) {
+    for (int x = EC_LANE; x < n_dep * M; x += EC_TSIZE) {
+      const int k = x / M, i = x - k * M + 1;
+      const int dp = w->dep_pos[k];
+      if (dp >= stop_p) continue;
+      int lo = w->ioff[i - 1], hi = w->ioff[i]; /* first entry with position >= dp */
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (w->ilist[mid] < dp)
+          lo = mid + 1;
+        else
+          hi = mid;
+      }
+      w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
     }
-    w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
+  } else {
+    snapshots_merge(w, n_dep, stop_p);
   }
   t_sync();
   for (int k = 0; k < n_dep; k++) {

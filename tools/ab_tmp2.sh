@@ -1,4 +1,3 @@
-for t in quad solo quad solo; do
-  r=$(ASB_TEAM=$t timeout 300 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('%.1f'%d['ms_per_step'], d['parity'])" 2>&1 | tail -1)
-  echo "team $t: $r"
-done
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
+timeout 600 python bench.py --config c4 --steps 2 --warmup 1 --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c4', d['ms_per_step'], '%.3g'%d['value'], d['parity'], 'cpu %.3g'%d['cpu_baseline']['value'])"
+timeout 600 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c5', d['ms_per_step'])"
