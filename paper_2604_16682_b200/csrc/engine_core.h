@@ -243,7 +243,8 @@ struct WS {
   long long hz_s;
   int n_alive, rr_next, arr_ptr, arr_rank, status, incl;
   int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i, n_dep;
-  int due_ready, n_cand, cand_token, n_empty;
+  int due_ready, n_cand, cand_token, n_empty, cand_collect;
+  int stamp_ctr; /* last due-list stamp handed out (dstamp de-duplication) */
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
   unsigned long long tmin[MAXM];
@@ -585,7 +586,9 @@ EC_COLD2 void cond_changed(W* w, const GP& g, int i) {
   }
   t_sync();
   if (w->flag) {
-    int cnt = log_pass(w, g, i, 1, w->seq, w->now);
+    /* re-timed turns that now fall inside the window become due candidates
+     * when a coupling follow-up keeps the batch's due list (cand_collect) */
+    int cnt = log_pass<W, W::DC>(w, g, i, 1, w->seq, w->now, w->cand_collect != 0);
     EC_LANE0 w->seq += cnt;
     t_sync();
   }
@@ -1026,10 +1029,12 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
  * minima into tmin (controller.py:89-103, engine.py:437-454), count the
  * ticks, and compact finished agents out lazily. */
 template <class W>
-EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int token) {
+EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int) {
   const int M = w->sc.n_instances;
   const int n = w->n_alive;
+  const int token = w->stamp_ctr + 1; /* a fresh stamp per due list */
   EC_LANE0 {
+    w->stamp_ctr = token;
     w->j_tick = 1;
     w->j_collect = collect;
     w->j_bound = bound;
@@ -1285,7 +1290,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   const int M = sc.n_instances;
   const bool collect = sc.interference == 0;
   EC_PROF_START(w);
-  tick_sweep(w, g, collect, w->bound, w->incl, (int)(k + 1));
+  tick_sweep(w, g, collect, w->bound, w->incl, 0);
   EC_PROF(w, 0);
   if (!collect) {
     epoch_serial(w, g, k);
@@ -1438,6 +1443,9 @@ EC_DEV int collect_due(W* w, const GP& g, double bound, int incl) {
     w->j_collect = 1;
     w->j_bound = bound;
     w->j_incl = incl;
+    /* a fresh stamp per due list: candidates added later (re-timed turns)
+     * are de-duplicated against this list only */
+    w->cand_token = ++w->stamp_ctr;
     w->j_token = w->cand_token;
     w->j_total = 0;
   }
@@ -2465,17 +2473,35 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   EC_LANE0 w->ctr[ASB_CTR_BATCHES]++;
   /* ---- 7. coupling / overflow follow-ups */
   const int stop = w->stop_kind;
+  /* the rest of the (unshrunk) window keeps this batch's due list: every
+   * agent with an event left in the window is one of them, or is re-timed
+   * by the coupling event's handler (collected as it happens) */
+  const bool keep = (bound == win_end && incl == w->incl) && w->n_due <= DCAP;
   if (stop == STOP_COUPLING) {
+    EC_LANE0 {
+      w->n_cand = w->n_due;
+      w->cand_collect = keep;
+    }
+    t_sync();
     exec_serial(w, g, w->stop_r); /* smem record: no local-memory copy */
+    EC_LANE0 {
+      w->cand_collect = 0;
+      w->due_ready = keep && w->n_cand <= DCAP;
+    }
+    t_sync();
     EC_PROF(w, 5);
     return BATCH_MORE;
   }
   EC_PROF(w, 5);
-  if (stop == STOP_LOGFULL) {
-    log_pass(w, g, w->stop_r.inst, 0, 0, w->now);
+  if (stop == STOP_LOGFULL || stop == STOP_HORIZON) {
+    if (stop == STOP_LOGFULL) log_pass(w, g, w->stop_r.inst, 0, 0, w->now);
+    EC_LANE0 {
+      w->n_cand = w->n_due;
+      w->due_ready = keep;
+    }
+    t_sync();
     return BATCH_MORE;
   }
-  if (stop == STOP_HORIZON) return BATCH_MORE;
   if (bound != win_end || incl != w->incl) {
     /* the shrunk window is fully committed: continue from its end */
     EC_LANE0 w->now = bound;
@@ -2569,7 +2595,8 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     w->start_ctr = 0;
     for (int c = 0; c < ASB_NCOUNTERS; c++) w->ctr[c] = 0;
     w->n_alive = w->rr_next = w->arr_ptr = w->arr_rank = w->status = 0;
-    w->due_ready = w->n_cand = w->cand_token = w->n_empty = 0;
+    w->due_ready = w->n_cand = w->cand_token = w->n_empty = w->cand_collect = 0;
+    w->stamp_ctr = 0;
     for (int c = 0; c < 6; c++) w->prof[c] = 0;
   }
   t_sync();
