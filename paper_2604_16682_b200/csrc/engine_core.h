@@ -268,6 +268,7 @@ struct WS {
   short sw_inst[RCAP];
   unsigned char sw_prio[RCAP], sw_flags[RCAP];
   int dep_pos[DEP];
+  int dep_target[DEP]; /* routed instance of each dependent arrival */
   long long snap[DEP][MAXM];
   long long carry_u;
   int carry_r, carry_l;
@@ -1569,6 +1570,78 @@ EC_COLD4 void snapshots_merge(W* w, int n_dep, int stop_p) {
   }
 }
 
+/* lane-serial argmin of (usage, id) over snapshot k (router.py:91,123,150):
+ * cand_mode 0 = all instances, 1 = reassignment candidates; 0 = none */
+template <class W>
+EC_DEV int snap_argmin_lane(const W* w, int k, bool all, int cur, long long* bu_out) {
+  const int M = w->sc.n_instances;
+  long long bu = 0;
+  int bi = 0;
+  for (int i = 1; i <= M; i++) {
+    const long long u = w->snap[k][i - 1];
+    if (!(all || u > 0 || i == cur)) continue;
+    if (!bi || u < bu) {
+      bu = u;
+      bi = i;
+    }
+  }
+  *bu_out = bu;
+  return bi;
+}
+
+/* reassignment checks of the dependent records before stop_p, one lane per
+ * check (each reads only its own usage snapshot): the position of the
+ * first that migrates (maybe_reassign, router.py:110-128), or stop_p */
+template <class W>
+EC_COLD4 int checks_parallel(const W* w, int n_dep, int stop_p) {
+  const AsbScenario& sc = w->sc;
+  const bool all = sc.include_idle;
+  int first = stop_p;
+  for (int k = EC_LANE; k < n_dep; k += EC_TSIZE) {
+    const int p = w->dep_pos[k];
+    if (p >= stop_p || w->sw_prio[p] != EV_TOOL) continue;
+    const int cur = w->sw_inst[p];
+    long long bu = 0;
+    const int bi = snap_argmin_lane(w, k, all, cur, &bu);
+    if (bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu && p < first) first = p;
+  }
+  return (int)t_redux_min_u32((unsigned)first);
+}
+
+/* arrival routing of the dependent records before stop_p, one lane per
+ * arrival (router.py:75-94,131-151 on its usage snapshot) into
+ * w->dep_target[k]; round-robin takes rr_next + its rank among the batch's
+ * arrivals */
+template <class W>
+EC_COLD4 void route_parallel(W* w, int n_dep, int stop_p) {
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances;
+  const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+  int before = 0; /* arrivals ahead of this lane's chunk */
+  for (int base = 0; base < n_dep; base += EC_TSIZE) {
+    const int k = base + EC_LANE;
+    const int p = k < n_dep ? w->dep_pos[k] : 0x7fffffff;
+    const bool arr = p < stop_p && w->sw_prio[p] == EV_ARRIVAL;
+    const unsigned m = t_ballot(arr);
+    if (arr) {
+      int target;
+      if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
+        target = (int)(((long long)w->rr_next + before + ec_popc(m & t_lt_mask())) % M) + 1;
+      } else {
+        int light = 0;
+        if (sc.policy == ASB_POLICY_CONTEXT_AWARE)
+          for (int i = 1; i <= M && !light; i++)
+            if ((double)w->snap[k][i - 1] < threshold) light = i;
+        long long bu = 0;
+        target = light ? light : snap_argmin_lane(w, k, true, 0, &bu);
+      }
+      w->dep_target[k] = target;
+    }
+    before += ec_popc(m);
+  }
+  t_sync();
+}
+
 /* snap_argmin for M up to 64: each lane folds its instances into one 32-bit
  * key, one warp reduction; -1 when a usage does not fit the key */
 template <class W>
@@ -1771,17 +1844,29 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     snapshots_merge(w, n_dep, stop_p);
   }
   t_sync();
-  for (int k = 0; k < n_dep; k++) {
-    const int p = w->dep_pos[k];
-    if (p >= stop_p) break;
-    if (w->sw_prio[p] != EV_TOOL) continue;
-    const int cur = w->sw_inst[p];
-    long long bu = 0;
-    const int bi = snap_argmin(w, k, 1, cur, &bu);
-    if (bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu) {
-      stop_p = p;
-      stop_kind = STOP_COUPLING;
-      break;
+  if (M > EC_TSIZE) {
+    /* many instances: one lane per check */
+    if (n_dep > 0) {
+      const int mig = checks_parallel(w, n_dep, stop_p);
+      if (mig < stop_p) {
+        stop_p = mig;
+        stop_kind = STOP_COUPLING;
+      }
+    }
+  } else {
+    /* few instances: one warp reduction per check, in order */
+    for (int k = 0; k < n_dep; k++) {
+      const int p = w->dep_pos[k];
+      if (p >= stop_p) break;
+      if (w->sw_prio[p] != EV_TOOL) continue;
+      const int cur = w->sw_inst[p];
+      long long bu = 0;
+      const int bi = snap_argmin(w, k, 1, cur, &bu);
+      if (bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu) {
+        stop_p = p;
+        stop_kind = STOP_COUPLING;
+        break;
+      }
     }
   }
   EC_WPROF(w, 2);
@@ -1874,33 +1959,49 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   t_sync();
   EC_WPROF(w, 4);
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
-  for (int k = 0; k < n_dep; k++) {
-    const int p = w->dep_pos[k];
-    if (p >= stop_p) break;
-    if (w->sw_prio[p] != EV_ARRIVAL) continue;
-    int target;
-    if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
-      target = (w->rr_next % M) + 1;
-    } else {
-      /* context_aware: lowest id below theta * cap, else argmin (router.py:85-90) */
-      int light = 0;
-      if (sc.policy == ASB_POLICY_CONTEXT_AWARE) {
-        const double threshold = sc.consolidation_threshold * (double)sc.capacity;
-        for (int base = 0; base < M && !light; base += EC_TSIZE) {
-          const int i = base + EC_LANE + 1;
-          const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
-          if (m) light = base + ec_ffs(m);
-        }
-      }
-      long long bu = 0;
-      target = light ? light : snap_argmin(w, k, 0, 0, &bu);
-    }
+  if (n_dep > 0 && M > EC_TSIZE) {
+    /* many instances: route every arrival in parallel, commit in order */
+    route_parallel(w, n_dep, stop_p);
     EC_LANE0 {
-      const Rec& r = w->rec[w->sw_idx[p]];
-      if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
-      commit_arrival(w, g, r.agent, target, (int)r.seq);
+      for (int k = 0; k < n_dep; k++) {
+        const int p = w->dep_pos[k];
+        if (p >= stop_p) break;
+        if (w->sw_prio[p] != EV_ARRIVAL) continue;
+        const Rec& r = w->rec[w->sw_idx[p]];
+        if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
+        commit_arrival(w, g, r.agent, w->dep_target[k], (int)r.seq);
+      }
     }
     t_sync();
+  } else {
+    for (int k = 0; k < n_dep; k++) {
+      const int p = w->dep_pos[k];
+      if (p >= stop_p) break;
+      if (w->sw_prio[p] != EV_ARRIVAL) continue;
+      int target;
+      if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
+        target = (w->rr_next % M) + 1;
+      } else {
+        /* context_aware: lowest id below theta * cap, else argmin (router.py:85-90) */
+        int light = 0;
+        if (sc.policy == ASB_POLICY_CONTEXT_AWARE) {
+          const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+          for (int base = 0; base < M && !light; base += EC_TSIZE) {
+            const int i = base + EC_LANE + 1;
+            const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
+            if (m) light = base + ec_ffs(m);
+          }
+        }
+        long long bu = 0;
+        target = light ? light : snap_argmin(w, k, 0, 0, &bu);
+      }
+      EC_LANE0 {
+        const Rec& r = w->rec[w->sw_idx[p]];
+        if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
+        commit_arrival(w, g, r.agent, target, (int)r.seq);
+      }
+      t_sync();
+    }
   }
   EC_LANE0 {
     w->seq += pushes;
