@@ -13,7 +13,7 @@ allreduce of the 8-double stats vector when N > 1.
   python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config c5|c3|c4]
 
 --config selects another BASELINE.json workload for the same line format:
-c3 = the DVFS sweep (8 fixed levels x 4 capacities x 8 seeds per GPU, 1
+c3 = the DVFS sweep (8 fixed levels x 4 capacities x 64 seeds per GPU, 1
 instance x ~1k agents, 12500 epochs), c4 = the 100k-agent thrashing regime
 (one scenario, 64 instances).  The driver's headline is the default (c5).
 
@@ -104,8 +104,8 @@ CONFIGS = {
                                         "{ctx-aware,round-robin} router x {ctx-aware,off} controller x tau {20,35}), "
                                         "16 instances x ~10k agents, 3600 s",
            "instances": 16, "epochs": 3600, "sim_duration_s": 3600.0},
-    "c3": {"seeds_per_gpu": 8, "desc": "C3 DVFS sweep shard: 256 scenarios/GPU (8 seeds x 8 fixed frequency levels "
-                                       "x 4 capacities {250k,500k,750k,1M}), 1 instance x ~1k agents, 12500 s",
+    "c3": {"seeds_per_gpu": 64, "desc": "C3 DVFS sweep: 2048 scenarios/GPU (64 seeds x 8 fixed frequency levels "
+                                        "x 4 capacities {250k,500k,750k,1M}), 1 instance x ~1k agents, 12500 s",
            "instances": 1, "epochs": 12500, "sim_duration_s": 12500.0},
     "c4": {"seeds_per_gpu": 1, "desc": "C4 long-tail thrashing regime: 1 scenario/GPU, ~100k agents with "
                                        "prefill growth 20/turn, 64 instances, context-aware without thrash avoidance, "
