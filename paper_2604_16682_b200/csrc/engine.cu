@@ -399,8 +399,8 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
    *  - few large scenarios (each gets an SM of its own anyway): a 16-warp
    *    team with 5x larger optimistic batches;
    *  - small scenarios (< 2k agents on average): a single warp, no fork-join
-   *    barriers, 64-record batches (their per-epoch work is a few events),
-   *    ~20 KB of shared memory so ~10 teams fit per SM;
+   *    barriers, 40-record batches (their per-epoch work is a few events),
+   *    ~15 KB of shared memory so ~14 teams fit per SM;
    *  - otherwise 4-warp teams, 4 per SM. */
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -414,10 +414,10 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   }
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16) {
-    if (solo) return launch_engine<16, 64, 32, 32, 32>(d_scen, n_scen, traces, tables, out, ws, st);
+    if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   }
-  if (solo) return launch_engine<64, 64, 32, 32, 32>(d_scen, n_scen, traces, tables, out, ws, st);
+  if (solo) return launch_engine<64, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
   return launch_engine<64, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
 }
 
