@@ -112,6 +112,7 @@ typedef struct AsbScenario {
   /* sim */
   double sim_duration;
   int64_t n_epochs;              /* #{k : k*epoch_length < sim_duration}, engine.py:306-309 */
+  double record_interval;        /* SimConfig.record_interval: sample events at k*interval, engine.py:310-313 */
 } AsbScenario;
 
 /* Trace pool: CSR of AgentTrace/TurnRecord (workload.py:83-116), shared by scenarios. */
@@ -153,6 +154,20 @@ typedef struct AsbDecision {
   int32_t deferred;
 } AsbDecision;
 
+/* TimeseriesRow, engine.py:91-101, as _mark_row writes it (engine.py:403-429).
+ * level_mhz is not stored: it is table.level(level_index).nominal_mhz. */
+typedef struct AsbTimeseriesRow {
+  double time;
+  double power_watts;
+  int64_t context_usage;
+  int32_t instance_id;
+  int32_t level_index;           /* 1-based */
+  int32_t pending_depth;
+  int32_t running_requests;
+  int32_t thrashing;
+  int32_t pad_;
+} AsbTimeseriesRow;
+
 /* Outputs.  Agent rows are in TRACE order (local agent index); arrival_rank
  * gives the reference's result order (engine.py:609, dict insertion order),
  * -1 for agents that never arrived inside the window. */
@@ -186,6 +201,17 @@ typedef struct AsbOutputs {
   const int64_t* turn_off;
   double* turn_issue;              /* NaN when the turn did not complete */
   double* turn_done;
+  /* optional (NULL to skip): timeseries rows in the reference's emission
+   * order, capacity [ts_off[s], ts_off[s+1]) per scenario, the number written
+   * in ts_count[s].  A scenario with rows enabled runs the engine's exact
+   * serial event loop (one event at a time, sample events included) instead
+   * of the optimistic batches: same results, far slower; meant for single
+   * runs that need the series.  A capacity of
+   *   n_instances * (2 + n_samples + n_epochs) + n_agents + 3 * n_turns
+   * can never overflow (one row per handler, engine.py:488-603). */
+  const int64_t* ts_off;
+  AsbTimeseriesRow* timeseries;
+  int64_t* ts_count;
 } AsbOutputs;
 
 /* per-scenario system metrics (SystemMetrics, metrics.py:37-46). NaN encodes None. */
@@ -210,7 +236,7 @@ int asb_abi_version(void);
  * n_instances * agent count (pending FIFOs and running logs). */
 size_t asb_workspace_bytes(int32_t n_scen, int64_t total_agents, int64_t total_ring_slots);
 
-/* Run all scenarios to completion (one warp per scenario, persistent grid).
+/* Run all scenarios to completion (one CTA team per scenario, persistent grid).
  * d_scen: device array of n_scen AsbScenario; max_instances = max
  * n_instances over the batch (<= 64). */
 int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_instances,
@@ -266,7 +292,7 @@ int asb_reduce_stats(const AsbStats* d_stats, const int64_t* d_counters, int32_t
                      double* d_red, void* stream);
 
 /* ABI self-check: writes sizeof of AsbScenario, AsbTracePool, AsbTablePool,
- * AsbOutputs, AsbDecision, AsbStats into out[0..5]; returns 6. */
+ * AsbOutputs, AsbDecision, AsbStats, AsbTimeseriesRow into out[0..6]; returns 7. */
 int asb_struct_sizes(int64_t* out);
 
 #ifdef __cplusplus

@@ -17,8 +17,10 @@
  * vectors produced by the reference itself (tests/golden/make_golden.py).
  *
  * Deliberate, result-preserving restatements (each argued in DESIGN.md):
- *  - `sample` events (engine.py:570-572) only emit timeseries rows and are
- *    not scheduled; they never change state and never tie with other kinds.
+ *  - `sample` events (engine.py:570-572) only emit timeseries rows; they are
+ *    scheduled only when the caller asks for rows (AsbOutputs.timeseries).
+ *    They never change state, and their priority (5) is the lowest, so they
+ *    do not change the order of the other events.
  *  - `min_throughput` of every instance is evaluated once at the start of
  *    the epoch event over the alive list: epoch processing of instance j
  *    never changes the in-process set or throughputs of instance i != j
@@ -37,7 +39,7 @@
 #endif
 
 /* event kinds and tie-break priorities, engine.py:48-54 */
-enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4 };
+enum { EV_EPOCH = 0, EV_COMPLETE = 1, EV_TOOL = 2, EV_ISSUE = 3, EV_ARRIVAL = 4, EV_SAMPLE = 5 };
 
 typedef struct {
   double t;
@@ -120,6 +122,10 @@ typedef struct {
   int32_t thr_flag;
   double thr_since, thr_time;
   int32_t key_valid, key_level, key_thr, key_run;
+  /* last timeseries row key, engine.py:405-414 */
+  int32_t row_valid, row_level, row_pending, row_running, row_thr;
+  int64_t row_usage;
+  double row_watts;
 } Inst;
 
 typedef struct {
@@ -151,6 +157,8 @@ typedef struct {
   double *turn_issue, *turn_done;
   int32_t arrival_rank;
   int32_t* rank;
+  AsbTimeseriesRow* ts; /* NULL: no rows */
+  int64_t ts_cap, ts_n;
 } Sim;
 
 static inline double lvl_pr(const Sim* s, int l) { return s->tb->prefill_rate[s->tbl0 + l - 1]; }
@@ -203,6 +211,38 @@ static void sync_thrash(Sim* s, Inst* in) {
     in->thr_flag = flag;
     s->ctr[ASB_CTR_THRASH_FLIPS]++;
   }
+}
+
+/* _mark_row, engine.py:403-429: a row when the instance's observable key
+ * changed since its last row (or always, when forced) */
+static void mark_row(Sim* s, int i, int force) {
+  if (!s->ts) return;
+  Inst* in = &s->in[i];
+  if (!force && in->row_valid && in->row_usage == in->usage && in->row_level == in->level &&
+      in->row_watts == in->watts && in->row_pending == in->fifo_len && in->row_running == in->running &&
+      in->row_thr == in->thrashing)
+    return;
+  in->row_valid = 1;
+  in->row_usage = in->usage;
+  in->row_level = in->level;
+  in->row_watts = in->watts;
+  in->row_pending = in->fifo_len;
+  in->row_running = in->running;
+  in->row_thr = in->thrashing;
+  if (s->ts_n >= s->ts_cap) {
+    s->status = ASB_SIMERR_OVERFLOW;
+    return;
+  }
+  AsbTimeseriesRow* r = &s->ts[s->ts_n++];
+  r->time = s->now;
+  r->power_watts = in->watts;
+  r->context_usage = in->usage;
+  r->instance_id = i;
+  r->level_index = in->level;
+  r->pending_depth = in->fifo_len;
+  r->running_requests = in->running;
+  r->thrashing = in->thrashing;
+  r->pad_ = 0;
 }
 
 /* _conditions_changed, engine.py:344-372 */
@@ -399,6 +439,7 @@ static void on_epoch(Sim* s, int64_t k) {
       d->boosted = boosted;
       d->deferred = deferred;
     }
+    mark_row(s, i, 0);
   }
 }
 
@@ -437,6 +478,7 @@ static void on_arrival(Sim* s, int32_t a) {
   fifo_append(&s->in[target], s, a);
   g->phase = ASB_PHASE_PENDING;
   alive_add(s, a);
+  mark_row(s, target, 0);
 }
 
 /* _on_complete, engine.py:509-535 */
@@ -476,6 +518,7 @@ static void on_complete(Sim* s, int32_t a, int64_t version) {
   sync_thrash(s, in);
   conditions_changed(s, in);
   update_power(s, in);
+  mark_row(s, g->inst, 0);
 }
 
 /* _on_tool, engine.py:537-561 with maybe_reassign router.py:97-128 */
@@ -505,6 +548,7 @@ static void on_tool(Sim* s, int32_t a) {
   Inst* src = &s->in[source];
   if (!target) {
     start_turn(s, src, a, s->now);
+    mark_row(s, source, 0);
     return;
   }
   Inst* dst = &s->in[target];
@@ -522,11 +566,14 @@ static void on_tool(Sim* s, int32_t a) {
   sync_thrash(s, src);
   conditions_changed(s, src);
   update_power(s, src);
+  mark_row(s, source, 0);
+  mark_row(s, target, 0);
 }
 
 static void on_issue(Sim* s, int32_t a, double issue) {
   s->ctr[ASB_CTR_EVENTS]++;
   start_turn(s, &s->in[s->ag[a].inst], a, issue);
+  mark_row(s, s->ag[a].inst, 0);
 }
 
 static int run_one(const AsbScenario* sc, const AsbTracePool* tp, const AsbTablePool* tb,
@@ -560,6 +607,10 @@ static int run_one(const AsbScenario* sc, const AsbTracePool* tp, const AsbTable
     int64_t nt = tp->trace_turn_off[sc->trace_id + 1] - tp->trace_turn_off[sc->trace_id];
     for (int64_t t = 0; t < nt; t++) s->turn_issue[t] = s->turn_done[t] = NAN;
   }
+  if (out->timeseries && out->ts_off && out->ts_count) {
+    s->ts = out->timeseries + out->ts_off[sidx];
+    s->ts_cap = out->ts_off[sidx + 1] - out->ts_off[sidx];
+  }
   for (int a = 0; a < A; a++) {
     Agent* g = &s->ag[a];
     g->turn0 = tp->agent_turn_off[s->a0 + a];
@@ -576,13 +627,18 @@ static int run_one(const AsbScenario* sc, const AsbTracePool* tp, const AsbTable
     in->run_head = in->run_tail = -1;
     in->watts = lvl_idle(s, L);
   }
-  /* _schedule_initial, engine.py:303-317 (samples omitted, see header) */
+  /* _schedule_initial, engine.py:303-317 (samples only with rows, see header) */
   double T = sc->sim_duration, E = sc->epoch_length;
   for (int64_t k = 0; k < sc->n_epochs; k++) push(s, (double)k * E, EV_EPOCH, (int32_t)k, 0, 0.0);
+  if (s->ts)
+    for (int64_t k = 1; (double)k * sc->record_interval < T; k++)
+      push(s, (double)k * sc->record_interval, EV_SAMPLE, 0, 0, 0.0);
   for (int a = 0; a < A; a++) {
     double arr = tp->arrival[s->a0 + a];
     if (arr < T) push(s, arr, EV_ARRIVAL, a, 0, 0.0);
   }
+  /* run(), engine.py:576-579: a forced row per instance at t = 0 */
+  for (int i = 1; i <= M; i++) mark_row(s, i, 1);
   /* hot loop, engine.py:589-594 */
   while (s->heap.n > 0 && s->status == 0) {
     Ev e = heap_pop(&s->heap);
@@ -594,6 +650,9 @@ static int run_one(const AsbScenario* sc, const AsbTracePool* tp, const AsbTable
       case EV_TOOL: on_tool(s, e.agent); break;
       case EV_ISSUE: on_issue(s, e.agent, e.issue); break;
       case EV_ARRIVAL: on_arrival(s, e.agent); break;
+      case EV_SAMPLE: /* _on_sample, engine.py:570-572 */
+        for (int i = 1; i <= M; i++) mark_row(s, i, 1);
+        break;
     }
   }
   /* final accounting, engine.py:595-603 */
@@ -606,7 +665,9 @@ static int run_one(const AsbScenario* sc, const AsbTracePool* tp, const AsbTable
       in->thr_time += T - in->thr_since;
       in->thr_since = T;
     }
+    mark_row(s, i, 1);
   }
+  if (s->ts) out->ts_count[sidx] = s->ts_n;
   /* outputs */
   for (int a = 0; a < A; a++) {
     const Agent* g = &s->ag[a];

@@ -50,10 +50,11 @@ def _structs(batch, arrays):
     return tp, tb, out
 
 
-def run_oracle(batch, decisions: bool = True, turn_log: bool = True, threads: int = 0, timing: dict | None = None):
+def run_oracle(batch, decisions: bool = True, turn_log: bool = True, threads: int = 0, timing: dict | None = None,
+               timeseries: bool = False):
     """Serial C oracle over every scenario; returns (outputs, stats)."""
     lib = _load(_build.build_oracle(), "oracle_run_scenarios", [C.c_int32])
-    arrays = alloc_host_outputs(batch, decisions, turn_log)
+    arrays = alloc_host_outputs(batch, decisions, turn_log, timeseries)
     tp, tb, out = _structs(batch, arrays)
     scen = np.ascontiguousarray(batch.scen)
     t0 = time.perf_counter()
@@ -65,11 +66,12 @@ def run_oracle(batch, decisions: bool = True, turn_log: bool = True, threads: in
     return arrays, stats
 
 
-def run_host_engine(batch, small_buffers: bool = False, decisions: bool = True, turn_log: bool = True):
+def run_host_engine(batch, small_buffers: bool = False, decisions: bool = True, turn_log: bool = True,
+                    timeseries: bool = False):
     """1-lane CPU build of the GPU engine core (test harness); returns (outputs, stats)."""
     lib = _load(_build.build_host_engine(), "host_engine_run", [C.c_int32])
     olib = _load(_build.build_oracle(), "oracle_run_scenarios", [C.c_int32])
-    arrays = alloc_host_outputs(batch, decisions, turn_log)
+    arrays = alloc_host_outputs(batch, decisions, turn_log, timeseries)
     tp, tb, out = _structs(batch, arrays)
     scen = np.ascontiguousarray(batch.scen)
     lib.host_engine_run(scen.ctypes.data, batch.n, C.byref(tp), C.byref(tb), C.byref(out), int(small_buffers))

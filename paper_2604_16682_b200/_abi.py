@@ -59,6 +59,7 @@ SCENARIO_DTYPE = np.dtype(
         ("migration_delay", "<f8"),
         ("sim_duration", "<f8"),
         ("n_epochs", "<i8"),
+        ("record_interval", "<f8"),
     ],
     align=True,
 )
@@ -74,6 +75,21 @@ DECISION_DTYPE = np.dtype(
         ("pending_depth", "<i4"),
         ("boosted", "<i4"),
         ("deferred", "<i4"),
+    ],
+    align=True,
+)
+
+TIMESERIES_DTYPE = np.dtype(
+    [
+        ("time", "<f8"),
+        ("power_watts", "<f8"),
+        ("context_usage", "<i8"),
+        ("instance_id", "<i4"),
+        ("level_index", "<i4"),
+        ("pending_depth", "<i4"),
+        ("running_requests", "<i4"),
+        ("thrashing", "<i4"),
+        ("pad_", "<i4"),
     ],
     align=True,
 )
@@ -149,6 +165,9 @@ class AsbOutputs(C.Structure):
         ("turn_off", P),
         ("turn_issue", P),
         ("turn_done", P),
+        ("ts_off", P),
+        ("timeseries", P),
+        ("ts_count", P),
     ]
 
 
@@ -179,7 +198,7 @@ INST_OUT = {
 def struct_sizes() -> list[int]:
     """Sizes in header order, as the C side reports them via asb_struct_sizes."""
     return [SCENARIO_DTYPE.itemsize, C.sizeof(AsbTracePool), C.sizeof(AsbTablePool), C.sizeof(AsbOutputs),
-            DECISION_DTYPE.itemsize, STATS_DTYPE.itemsize]
+            DECISION_DTYPE.itemsize, STATS_DTYPE.itemsize, TIMESERIES_DTYPE.itemsize]
 
 
 def make_outputs(ptr_of, arrays: dict) -> AsbOutputs:

@@ -328,12 +328,19 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 4 : 1)
     g.o_pending = out.final_pending + oi;
     g.o_level = out.final_level + oi;
     g.o_ctr = reinterpret_cast<long long*>(out.counters) + (long long)s * ASB_NCOUNTERS;
+    const bool ts_on = out.timeseries && out.ts_off && out.ts_off[s + 1] > out.ts_off[s];
+    g.ts_rows = ts_on ? out.timeseries + out.ts_off[s] : nullptr;
+    g.ts_cap = ts_on ? out.ts_off[s + 1] - out.ts_off[s] : 0;
+    g.ts_count = out.ts_count ? reinterpret_cast<long long*>(out.ts_count) + s : nullptr;
     g.A = A;
     g.M = sc.n_instances;
     g.L = sc.n_levels;
     if (EC_LANE == 0) w->gp = g;
     __syncwarp();
-    asb::run_scenario<W, RCAP, DCAP, ACAP>(w, w->gp); /* smem copy: no local-memory GP */
+    if (ts_on) /* smem copy of GP: no local-memory frame */
+      asb::run_scenario<W, RCAP, DCAP, ACAP, true>(w, w->gp);
+    else
+      asb::run_scenario<W, RCAP, DCAP, ACAP, false>(w, w->gp);
     __syncwarp();
   }
   if (EC_LANE == 0) w->job = asb::JOB_EXIT;

@@ -193,6 +193,10 @@ struct GP {
   long long* o_usage;
   int *o_pending, *o_level;
   long long* o_ctr;
+  /* timeseries rows (NULL: off; then the scenario runs the exact serial loop) */
+  AsbTimeseriesRow* ts_rows;
+  long long ts_cap;
+  long long* ts_count;
   int A, M, L;
 };
 
@@ -276,6 +280,9 @@ struct WS {
   Rec stop_r;
   long long prof[6];
   long long prof_t;
+  /* timeseries: rows written, next sample index, each instance's last row */
+  long long ts_n, ts_k;
+  long long ts_last[MAXM];
 };
 
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
@@ -426,6 +433,56 @@ EC_DEV void sync_thrash(W* w, int i, double now) {
     else
       in.thr_since = now;
     in.thr_flag = in.thr;
+  }
+}
+
+/* _mark_row, engine.py:403-429 (one lane): a row when the instance's key
+ * (usage, level, watts, pending, running, thrashing) differs from its last
+ * row's, or always when forced (samples, start and end of the run) */
+template <class W>
+EC_COLD4 void mark_row(W* w, const GP& g, int i, double now, bool force) {
+  const Inst& in = w->in[i - 1];
+  const long long last = w->ts_last[i - 1];
+  if (!force && last >= 0) {
+    const AsbTimeseriesRow& p = g.ts_rows[last];
+    if (p.context_usage == in.usage && p.level_index == in.level && p.power_watts == in.watts &&
+        p.pending_depth == in.fifo_len && p.running_requests == in.running && p.thrashing == in.thr)
+      return;
+  }
+  if (w->ts_n >= g.ts_cap) {
+    w->status = ASB_SIMERR_OVERFLOW;
+    return;
+  }
+  AsbTimeseriesRow& r = g.ts_rows[w->ts_n];
+  r.time = now;
+  r.power_watts = in.watts;
+  r.context_usage = in.usage;
+  r.instance_id = i;
+  r.level_index = in.level;
+  r.pending_depth = in.fifo_len;
+  r.running_requests = in.running;
+  r.thrashing = in.thr;
+  r.pad_ = 0;
+  w->ts_last[i - 1] = w->ts_n++;
+}
+
+/* the handler's row (engine.py:488, 507, 535, 549, 560, 568), lane 0 */
+template <class W>
+EC_DEV void ts_mark(W* w, const GP& g, int i) {
+  if (g.ts_rows) mark_row(w, g, i, w->now, false);
+}
+
+/* _on_sample (engine.py:570-572): flush every sample event k*interval that
+ * precedes `limit` (samples have the lowest priority: a sample at t runs
+ * after every event at t), lane 0 */
+template <class W>
+EC_COLD4 void ts_samples(W* w, const GP& g, double limit) {
+  const double iv = w->sc.record_interval, T = w->sc.sim_duration;
+  for (;;) {
+    const double st = (double)w->ts_k * iv;
+    if (!(st < limit && st < T) || w->status) break;
+    for (int i = 1; i <= w->sc.n_instances; i++) mark_row(w, g, i, st, true);
+    w->ts_k++;
   }
 }
 
@@ -688,7 +745,10 @@ EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
   }
   t_sync();
   cond_changed(w, g, i);
-  EC_LANE0 update_power(w, i, w->now);
+  EC_LANE0 {
+    update_power(w, i, w->now);
+    ts_mark(w, g, i);
+  }
   t_sync();
 }
 
@@ -731,10 +791,16 @@ EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
   t_sync();
   if (!w->flag) {
     start_turn_serial(w, g, source, a, w->now);
+    EC_LANE0 ts_mark(w, g, source);
+    t_sync();
     return;
   }
   cond_changed(w, g, source);
-  EC_LANE0 update_power(w, source, w->now);
+  EC_LANE0 {
+    update_power(w, source, w->now);
+    ts_mark(w, g, source);
+    ts_mark(w, g, g.H[a].inst); /* the target, engine.py:560-561 */
+  }
   t_sync();
 }
 
@@ -750,7 +816,10 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
   } else {
     EC_LANE0 w->ctr[ASB_CTR_EVENTS]++;
     t_sync();
-    start_turn_serial(w, g, g.H[r.agent].inst, r.agent, g.H[r.agent].issue);
+    const int i = g.H[r.agent].inst;
+    start_turn_serial(w, g, i, r.agent, g.H[r.agent].issue);
+    EC_LANE0 ts_mark(w, g, i); /* _on_delayed_start, engine.py:563-568 */
+    t_sync();
   }
 }
 
@@ -1277,6 +1346,7 @@ EC_COLD2 void epoch_serial(W* w, const GP& g, long long k) {
     EC_LANE0 {
       update_power(w, i, w->now);
       write_decision(w, g, k, i);
+      ts_mark(w, g, i);
     }
     t_sync();
   }
@@ -1289,7 +1359,7 @@ template <class W, int DCAP>
 EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances;
-  const bool collect = sc.interference == 0;
+  const bool collect = sc.interference == 0 && !g.ts_rows;
   EC_PROF_START(w);
   tick_sweep(w, g, collect, w->bound, w->incl, 0);
   EC_PROF(w, 0);
@@ -2657,10 +2727,16 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   if (arr < 0 && ba < 0) return false;
   double t = arr >= 0 ? g.arrival[arr] : ec_from_bits(bt);
   if (!(w->incl ? t <= win_end : t < win_end)) return false;
+  if (g.ts_rows) {
+    EC_LANE0 ts_samples(w, g, t);
+    t_sync();
+  }
   if (arr >= 0) {
     EC_LANE0 {
       w->now = t;
-      commit_arrival(w, g, arr, route_arrival(w), w->arr_ptr);
+      const int target = route_arrival(w);
+      commit_arrival(w, g, arr, target, w->arr_ptr);
+      ts_mark(w, g, target);
     }
     t_sync();
     return true;
@@ -2674,7 +2750,10 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   return true;
 }
 
-template <class W, int RCAP, int DCAP, int ACAP>
+/* TS: the scenario writes timeseries rows (g.ts_rows) and runs the exact
+ * serial loop; a separate instantiation keeps the batched engine's code
+ * unchanged */
+template <class W, int RCAP, int DCAP, int ACAP, bool TS>
 EC_DEV void run_scenario(W* w, const GP& g) {
   const AsbScenario& sc = w->sc;
   const int M = sc.n_instances, L = sc.n_levels;
@@ -2699,6 +2778,13 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     w->due_ready = w->n_cand = w->cand_token = w->n_empty = w->cand_collect = 0;
     w->stamp_ctr = 0;
     for (int c = 0; c < 6; c++) w->prof[c] = 0;
+    if (TS) {
+      w->ts_n = 0;
+      w->ts_k = 1;
+      for (int i = 0; i < M; i++) w->ts_last[i] = -1;
+      /* run(), engine.py:576-579: a forced row per instance before any event */
+      for (int i = 1; i <= M; i++) mark_row(w, g, i, 0.0, true);
+    }
   }
   t_sync();
   const long long K = sc.n_epochs;
@@ -2734,6 +2820,17 @@ EC_DEV void run_scenario(W* w, const GP& g) {
         t_sync();
         break;
       }
+      if (TS) {
+        /* timeseries: the exact serial loop, one event at a time (each step
+         * executes an event, so the watchdog does not apply) */
+        guard++;
+        if (!serial_step(w, g, win_end)) {
+          EC_LANE0 ts_samples(w, g, win_end);
+          t_sync();
+          break;
+        }
+        continue;
+      }
       int rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);
       if (rc == BATCH_MORE) continue;
       if (rc == BATCH_DONE) break;
@@ -2755,6 +2852,15 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     g.o_usage[i] = in.usage;
     g.o_pending[i] = in.fifo_len;
     g.o_level[i] = in.level;
+  }
+  if (TS) {
+    t_sync();
+    EC_LANE0 {
+      /* engine.py:595-603: a forced row per instance at the end */
+      for (int i = 1; i <= M; i++) mark_row(w, g, i, T, true);
+      if (g.ts_count) *g.ts_count = w->ts_n;
+    }
+    t_sync();
   }
   fork_job(w, JOB_FINISH);
   EC_LANE0 {

@@ -374,7 +374,8 @@ int asb_struct_sizes(int64_t* out4) {  /* NOLINT */
   out4[3] = (int64_t)sizeof(AsbOutputs);
   out4[4] = (int64_t)sizeof(AsbDecision);
   out4[5] = (int64_t)sizeof(AsbStats);
-  return 6;
+  out4[6] = (int64_t)sizeof(AsbTimeseriesRow);
+  return 7;
 }
 
 }  // extern "C"

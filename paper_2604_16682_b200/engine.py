@@ -7,9 +7,11 @@ the GPU (one warp per scenario) and rebuild the reference's result objects.
 ``DeviceBatch`` keeps a packed batch resident in HBM for repeated runs (the
 benchmark's timed region).
 
-Not produced on the device (SURVEY §8f "next", rank 3): the timeseries rows
-of ``_mark_row`` (engine.py:403-429); ``SimulationResult.timeseries`` is an
-empty list.
+Timeseries rows (``_mark_row``, engine.py:403-429) are produced on the
+device when asked for (``timeseries=True``, the default of
+``run_simulation``): those scenarios run the engine's exact serial event
+loop, sample events included, instead of the optimistic batches.  Batches
+default to ``timeseries=False`` (``SimulationResult.timeseries`` empty).
 """
 
 from __future__ import annotations
@@ -276,7 +278,8 @@ def prepare_batch(configs: Sequence[SimConfig]) -> packing.Batch:
     return packing.build_batch(scen, packing.pack_traces(trace_arrays), packing.pack_tables(tables))
 
 
-def alloc_host_outputs(batch: packing.Batch, decisions: bool = True, turn_log: bool = True) -> dict:
+def alloc_host_outputs(batch: packing.Batch, decisions: bool = True, turn_log: bool = True,
+                       timeseries: bool = False) -> dict:
     """numpy output buffers matching AsbOutputs (used by host-side checkers)."""
     arrays = {"agent_off": batch.agent_off, "inst_off": batch.inst_off}
     for k, dt in _abi.AGENT_OUT.items():
@@ -292,6 +295,10 @@ def alloc_host_outputs(batch: packing.Batch, decisions: bool = True, turn_log: b
         arrays["turn_off"] = batch.turn_off
         arrays["turn_issue"] = np.zeros(int(batch.turn_off[-1]), dtype=np.float64)
         arrays["turn_done"] = np.zeros(int(batch.turn_off[-1]), dtype=np.float64)
+    if timeseries:
+        arrays["ts_off"] = batch.ts_off
+        arrays["timeseries"] = np.zeros(int(batch.ts_off[-1]), dtype=_abi.TIMESERIES_DTYPE)
+        arrays["ts_count"] = np.zeros(batch.n, dtype=np.int64)
     return arrays
 
 
@@ -302,7 +309,8 @@ class DeviceBatch:
     fold on the current stream (no host sync); ``download()`` copies back.
     """
 
-    def __init__(self, batch: packing.Batch, device=None, decisions: bool = False, turn_log: bool = False):
+    def __init__(self, batch: packing.Batch, device=None, decisions: bool = False, turn_log: bool = False,
+                 timeseries: bool = False):
         import torch
 
         from . import _native, ops  # noqa: F401  (registers the custom ops)
@@ -335,6 +343,13 @@ class DeviceBatch:
                 outs[name] = torch.empty(nbytes, dtype=tdt, device=dev)
             elif name == "turn_off":
                 outs[name] = up(batch.turn_off) if turn_log else torch.empty(0, dtype=tdt, device=dev)
+            elif name == "ts_off":
+                outs[name] = up(batch.ts_off) if timeseries else torch.empty(0, dtype=tdt, device=dev)
+            elif name == "timeseries":
+                nbytes = int(batch.ts_off[-1]) * _abi.TIMESERIES_DTYPE.itemsize if timeseries else 0
+                outs[name] = torch.empty(nbytes, dtype=tdt, device=dev)
+            elif name == "ts_count":
+                outs[name] = torch.zeros(batch.n if timeseries else 0, dtype=tdt, device=dev)
             else:  # turn_issue / turn_done
                 n = int(batch.turn_off[-1]) if turn_log else 0
                 outs[name] = torch.empty(n, dtype=tdt, device=dev)
@@ -367,6 +382,11 @@ class DeviceBatch:
             host.pop("dec_off")
         if not host["turn_issue"].size and int(self.batch.turn_off[-1]):
             for k in ("turn_off", "turn_issue", "turn_done"):
+                host.pop(k)
+        if host["ts_count"].size:
+            host["timeseries"] = host["timeseries"].view(_abi.TIMESERIES_DTYPE)
+        else:
+            for k in ("ts_off", "timeseries", "ts_count"):
                 host.pop(k)
         stats = self.stats.cpu().numpy().view(_abi.STATS_DTYPE)
         return host, stats
@@ -447,6 +467,18 @@ def build_results(batch: packing.Batch, host: Mapping, stats: np.ndarray, config
                             int(r["pending_depth"]))
                 for r in rows
             ]
+        timeseries = []
+        if "timeseries" in host:
+            t0 = int(batch.ts_off[s])
+            rows = host["timeseries"][t0: t0 + int(host["ts_count"][s])]
+            table = cfg.instance.frequency_table
+            timeseries = [
+                TimeseriesRow(float(r["time"]), int(r["instance_id"]), int(r["context_usage"]),
+                              int(r["level_index"]), float(table.level(int(r["level_index"])).nominal_mhz),
+                              float(r["power_watts"]), int(r["pending_depth"]), int(r["running_requests"]),
+                              int(r["thrashing"]))
+                for r in rows
+            ]
         st = stats[s]
         ctr = ctr_all[s]
         system = SystemMetrics(
@@ -466,7 +498,7 @@ def build_results(batch: packing.Batch, host: Mapping, stats: np.ndarray, config
                 arrived=int(ctr[_abi.CTR["arrived"]]),
                 completed=int(ctr[_abi.CTR["completed"]]),
                 agents=agents,
-                timeseries=[],
+                timeseries=timeseries,
                 decisions=decisions,
                 instance_energy={i + 1: float(host["energy"][i0 + i]) for i in range(m)},
                 instance_thrash_time={i + 1: float(host["thrash_time"][i0 + i]) for i in range(m)},
@@ -481,19 +513,23 @@ def build_results(batch: packing.Batch, host: Mapping, stats: np.ndarray, config
 
 
 def run_simulation_batch(configs: Sequence[SimConfig], config_echos: Sequence[dict | None] | None = None, *,
-                         device=None, decisions: bool = True, turn_log: bool = True) -> list[SimulationResult]:
+                         device=None, decisions: bool = True, turn_log: bool = True,
+                         timeseries: bool = False) -> list[SimulationResult]:
     """Run many independent simulations on one GPU; each result equals the
-    reference's ``run_simulation`` of the same config."""
+    reference's ``run_simulation`` of the same config (``timeseries`` rows
+    only when asked for: those scenarios take the exact serial loop)."""
     batch = prepare_batch(configs)
-    dev_batch = DeviceBatch(batch, device=device, decisions=decisions, turn_log=turn_log)
+    dev_batch = DeviceBatch(batch, device=device, decisions=decisions, turn_log=turn_log, timeseries=timeseries)
     dev_batch.run()
     host, stats = dev_batch.download()
     return build_results(batch, host, stats, configs, config_echos)
 
 
-def run_simulation(config: SimConfig, config_echo: dict | None = None) -> SimulationResult:
-    """Run one simulation (engine.py:752-754) on the B200 engine."""
-    return run_simulation_batch([config], [config_echo])[0]
+def run_simulation(config: SimConfig, config_echo: dict | None = None, *, timeseries: bool = True) -> SimulationResult:
+    """Run one simulation (engine.py:752-754) on the B200 engine, timeseries
+    rows included like the reference's (``timeseries=False`` skips them and
+    takes the optimistic-batch engine)."""
+    return run_simulation_batch([config], [config_echo], timeseries=timeseries)[0]
 
 
 def agent_ticks_closed_form(arrival: np.ndarray, completion: np.ndarray, epoch_length: float,

@@ -27,6 +27,9 @@ OUT_ORDER = (
     ("turn_off", torch.int64),
     ("turn_issue", torch.float64),
     ("turn_done", torch.float64),
+    ("ts_off", torch.int64),
+    ("timeseries", torch.uint8),
+    ("ts_count", torch.int64),
 )
 OUT_NAMES = tuple(k for k, _ in OUT_ORDER)
 

@@ -198,7 +198,25 @@ def scenario_record(config, trace_id: int, table_id: int) -> tuple:
     rec["migration_delay"] = rt.migration_delay
     rec["sim_duration"] = config.sim_duration
     rec["n_epochs"] = epoch_count(config.sim_duration, ctl.epoch_length)
+    rec["record_interval"] = config.record_interval
     return rec
+
+
+def sample_count(sim_duration: float, record_interval: float) -> int:
+    """#{k >= 1 : k * record_interval < sim_duration}: the sample events of
+    _schedule_initial (engine.py:310-313)."""
+    return max(epoch_count(sim_duration, record_interval) - 1, 0)
+
+
+def timeseries_capacity(scen: np.ndarray, a_cnt: np.ndarray, t_cnt: np.ndarray) -> np.ndarray:
+    """Per-scenario row bound that _mark_row can never exceed: one row per
+    instance at start, end, every sample and every epoch (engine.py:488, 572,
+    579, 603) plus at most one per arrival, per completion, per tool event and
+    per delayed start (each <= turns; engine.py:507, 535, 549/561, 568)."""
+    m = scen["n_instances"].astype(np.int64)
+    samples = np.array([sample_count(float(r["sim_duration"]), float(r["record_interval"])) for r in scen],
+                       dtype=np.int64).reshape(-1)
+    return m * (2 + samples + scen["n_epochs"].astype(np.int64)) + a_cnt + 3 * t_cnt
 
 
 @dataclass
@@ -212,6 +230,7 @@ class Batch:
     inst_off: np.ndarray      # i64[n+1]
     dec_off: np.ndarray       # i64[n+1]
     turn_off: np.ndarray      # i64[n+1]
+    ts_off: np.ndarray        # i64[n+1] timeseries row capacity (timeseries_capacity)
     total_agents: int
     total_ring: int
     max_instances: int
@@ -241,6 +260,7 @@ def build_batch(scen: np.ndarray, traces: TracePool, tables: TablePool) -> Batch
         inst_off=offs(m),
         dec_off=offs(m * scen["n_epochs"].astype(np.int64)),
         turn_off=offs(t_cnt),
+        ts_off=offs(timeseries_capacity(scen, a_cnt, t_cnt)) if n else np.zeros(1, dtype=np.int64),
         total_agents=int(a_cnt.sum()),
         total_ring=int((m * a_cnt).sum()),
         max_instances=int(m.max()) if n else 1,

@@ -67,6 +67,7 @@ def config_from_dict(mod, d: dict, traces):
         controller=ctl,
         router=rt,
         sim_duration=d.get("duration", 3600.0),
+        record_interval=d.get("record_interval", 1.0),
     )
 
 
@@ -107,6 +108,12 @@ def canonical(result) -> dict:
                    _f(result.system.job_throughput), _f(result.system.average_power), _f(result.system.energy),
                    _f(result.system.thrash_fraction)],
     }
+
+
+def canonical_timeseries(result) -> list:
+    """SimulationResult.timeseries (engine.py:91-101) in a comparable form."""
+    return [[_f(r.time), r.instance_id, r.context_usage, r.level_index, _f(r.level_mhz), _f(r.power_watts),
+             r.pending_depth, r.running_requests, int(r.thrashing)] for r in result.timeseries]
 
 
 def digest(obj) -> str:
@@ -172,10 +179,10 @@ def close_difference(a, b, rel=1e-5, path="") -> str | None:
 # --------------------------------------------------------------------------- runners over a batch
 
 
-def results_via(runner, configs, decisions=True, turn_log=True):
+def results_via(runner, configs, decisions=True, turn_log=True, timeseries=False):
     """Run configs through a host runner (oracle / host engine) and rebuild results."""
     batch = prepare_batch(configs)
-    host, stats = runner(batch)
+    host, stats = runner(batch, timeseries=True) if timeseries else runner(batch)
     return build_results(batch, host, stats, configs, None), host
 
 

@@ -115,11 +115,18 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.o_pending = out->final_pending + oi;
     g.o_level = out->final_level + oi;
     g.o_ctr = (long long*)out->counters + (long long)s * ASB_NCOUNTERS;
+    const bool ts_on = out->timeseries && out->ts_off && out->ts_off[s + 1] > out->ts_off[s];
+    g.ts_rows = ts_on ? out->timeseries + out->ts_off[s] : nullptr;
+    g.ts_cap = ts_on ? out->ts_off[s + 1] - out->ts_off[s] : 0;
+    g.ts_count = out->ts_count ? (long long*)out->ts_count + s : nullptr;
     g.A = A;
     g.M = sc.n_instances;
     g.L = sc.n_levels;
     w->gp = g;
-    asb::run_scenario<W, RCAP, DCAP, ACAP>(w, g);
+    if (ts_on)
+      asb::run_scenario<W, RCAP, DCAP, ACAP, true>(w, g);
+    else
+      asb::run_scenario<W, RCAP, DCAP, ACAP, false>(w, g);
     err |= (int)g.o_ctr[ASB_CTR_STATUS];
     free(f64);
     free(hot);
