@@ -201,7 +201,7 @@ struct GP {
 };
 
 enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
-       JOB_EPOCH = 7, JOB_FINISH = 8 };
+       JOB_EPOCH = 7, JOB_FINISH = 8, JOB_DEPS = 9 };
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR>
 struct WS {
@@ -272,7 +272,8 @@ struct WS {
   short sw_inst[RCAP];
   unsigned char sw_prio[RCAP], sw_flags[RCAP];
   int dep_pos[DEP];
-  int dep_target[DEP]; /* routed instance of each dependent arrival */
+  int dep_target[DEP]; /* routed instance of each dependent arrival; -1: a migrating check (JOB_DEPS) */
+  int j_stop;          /* JOB_DEPS: records at or after this position are not committed */
   long long snap[DEP][MAXM];
   long long carry_u;
   int carry_r, carry_l;
@@ -1779,6 +1780,62 @@ EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_
   return bi;
 }
 
+/* JOB_DEPS (team, M > 32): the dependent records' usage snapshots, one
+ * binary search per (record, instance) pair across all threads; then one
+ * warp per record: the reassignment check (dep_target[k] = -1 when it
+ * migrates, maybe_reassign router.py:110-128) or the arrival's routing
+ * (router.py:75-94,131-151; round-robin is left to the in-order commit) */
+template <class W>
+EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
+  (void)g;
+  const AsbScenario& sc = w->sc;
+  const int M = sc.n_instances, n_dep = w->n_dep, stop_p = w->j_stop;
+  for (int x = tid; x < n_dep * M; x += nthr) {
+    const int k = x / M, i = x - k * M + 1;
+    const int dp = w->dep_pos[k];
+    if (dp >= stop_p) continue;
+    int lo = w->ioff[i - 1], hi = w->ioff[i]; /* first entry with position >= dp */
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (w->ilist[mid] < dp)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
+  }
+  ec_team_barrier();
+  const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+  for (int k = tid >> 5; k < n_dep; k += nthr >> 5) {
+    const int p = w->dep_pos[k];
+    if (p >= stop_p) continue;
+    const int pr = w->sw_prio[p];
+    long long bu = 0;
+    if (pr == EV_TOOL) {
+      const int cur = w->sw_inst[p];
+      const int bi = snap_argmin(w, k, 1, cur, &bu);
+      const bool mig = bi && bi != cur && (double)w->snap[k][cur - 1] >= sc.imbalance_ratio * (double)bu;
+      if (EC_LANE == 0) w->dep_target[k] = mig ? -1 : 0;
+    } else if (pr == EV_ARRIVAL && sc.policy != ASB_POLICY_ROUND_ROBIN) {
+      int light = 0;
+      if (sc.policy == ASB_POLICY_CONTEXT_AWARE)
+        for (int base = 0; base < M && !light; base += 32) {
+          const int i = base + EC_LANE + 1;
+          const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
+          if (m) light = base + ec_ffs(m);
+        }
+      const int target = light ? light : snap_argmin(w, k, 0, 0, &bu);
+      if (EC_LANE == 0) w->dep_target[k] = target;
+    }
+  }
+}
+
+/* M > 32: reassignment checks and arrival routing one lane per record
+ * (1) or one warp reduction per record, in order (0) */
+#ifndef EC_WIDE_LANE_PAR
+#define EC_WIDE_LANE_PAR 1
+#endif
+
 /* Parallel commit walk (team).  The serial walk's state machine decomposes
  * by instance: usage, running count, thrash flag, power and the running log
  * of instance i change only at records on i.  Each lane owns instances and
@@ -1895,7 +1952,23 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
    * one binary search per (record, instance) pair across the lanes; many
    * instances (M > 32): lane per instance, merging its sorted record list
    * with the sorted dependent positions */
-  if (M <= EC_TSIZE) {
+  const bool team_deps = W::NW > 1 && M > EC_TSIZE && n_dep > 0;
+  if (team_deps) {
+    /* many instances, helper warps: snapshots, checks and routing as a team job */
+    EC_LANE0 w->j_stop = stop_p;
+    t_sync();
+    fork_job(w, JOB_DEPS);
+    int mig = stop_p;
+    for (int k = EC_LANE; k < n_dep; k += EC_TSIZE) {
+      const int p = w->dep_pos[k];
+      if (p < stop_p && w->sw_prio[p] == EV_TOOL && w->dep_target[k] < 0 && p < mig) mig = p;
+    }
+    mig = (int)t_redux_min_u32((unsigned)mig);
+    if (mig < stop_p) {
+      stop_p = mig;
+      stop_kind = STOP_COUPLING;
+    }
+  } else if (M <= EC_TSIZE) {
     for (int x = EC_LANE; x < n_dep * M; x += EC_TSIZE) {
       const int k = x / M, i = x - k * M + 1;
       const int dp = w->dep_pos[k];
@@ -1914,7 +1987,9 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     snapshots_merge(w, n_dep, stop_p);
   }
   t_sync();
-  if (M > EC_TSIZE) {
+  if (team_deps) {
+    /* done by JOB_DEPS */
+  } else if (EC_WIDE_LANE_PAR && M > EC_TSIZE) {
     /* many instances: one lane per check */
     if (n_dep > 0) {
       const int mig = checks_parallel(w, n_dep, stop_p);
@@ -2029,17 +2104,22 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   t_sync();
   EC_WPROF(w, 4);
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
-  if (n_dep > 0 && M > EC_TSIZE) {
-    /* many instances: route every arrival in parallel, commit in order */
-    route_parallel(w, n_dep, stop_p);
+  if (EC_WIDE_LANE_PAR && n_dep > 0 && M > EC_TSIZE) {
+    /* many instances: route every arrival in parallel (JOB_DEPS or a lane
+     * per arrival), commit in order */
+    if (!team_deps) route_parallel(w, n_dep, stop_p);
     EC_LANE0 {
       for (int k = 0; k < n_dep; k++) {
         const int p = w->dep_pos[k];
         if (p >= stop_p) break;
         if (w->sw_prio[p] != EV_ARRIVAL) continue;
         const Rec& r = w->rec[w->sw_idx[p]];
-        if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next++;
-        commit_arrival(w, g, r.agent, w->dep_target[k], (int)r.seq);
+        int target = w->dep_target[k];
+        if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
+          target = (w->rr_next % M) + 1;
+          w->rr_next++;
+        }
+        commit_arrival(w, g, r.agent, target, (int)r.seq);
       }
     }
     t_sync();
@@ -2496,6 +2576,7 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
     case JOB_ADMIT: job_admit(w, g, tid, nthr); break;
     case JOB_EPOCH: job_epoch(w, g, tid, nthr); break;
     case JOB_FINISH: job_finish(w, g, tid, nthr); break;
+    case JOB_DEPS: job_deps(w, g, tid, nthr); break;
     default: break;
   }
 }

@@ -141,8 +141,11 @@ def test_c5_size_independent_properties(cuda_device):
         assert ctr[s, _abi.CTR["ticks"]] == want
 
 
-def test_wide_scenarios_64_instance_team(cuda_device):
-    """Scenarios with 17..64 instances run on the MAXM=64 small-team kernel."""
+@pytest.mark.parametrize("team", [None, "quad", "big"], indirect=True)
+def test_wide_scenarios_64_instance_team(cuda_device, team):
+    """Scenarios with 17..64 instances on the MAXM=64 kernels: the solo warp
+    (default for these sizes) and the multi-warp teams, whose walk runs the
+    snapshots / checks / routing of more than 32 instances as a team job."""
     import random as _random
 
     rng = _random.Random(5)
