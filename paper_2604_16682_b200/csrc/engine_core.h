@@ -208,6 +208,7 @@ struct WS {
   static constexpr int NT = NTHR;          /* threads of the team (main warp + helpers) */
   static constexpr int NW = (NTHR + 31) / 32;
   static constexpr int RC = RCAP, DC = DCAP, AC = ACAP;
+  static constexpr int MX = MAXM;          /* instance capacity of the kernel */
   /* large-batch teams: more dependent records per walk, and the apply
    * reloads agent state instead of caching it in shared memory */
   static constexpr int DEP = RCAP >= 512 ? 64 : EC_DEPCAP;
@@ -1952,7 +1953,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
    * one binary search per (record, instance) pair across the lanes; many
    * instances (M > 32): lane per instance, merging its sorted record list
    * with the sorted dependent positions */
-  const bool team_deps = W::NW > 1 && M > EC_TSIZE && n_dep > 0;
+  const bool team_deps = W::NW > 1 && W::MX > 32 && M > EC_TSIZE && n_dep > 0;
   if (team_deps) {
     /* many instances, helper warps: snapshots, checks and routing as a team job */
     EC_LANE0 w->j_stop = stop_p;
@@ -2576,7 +2577,9 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
     case JOB_ADMIT: job_admit(w, g, tid, nthr); break;
     case JOB_EPOCH: job_epoch(w, g, tid, nthr); break;
     case JOB_FINISH: job_finish(w, g, tid, nthr); break;
-    case JOB_DEPS: job_deps(w, g, tid, nthr); break;
+    case JOB_DEPS:
+      if (W::MX > 32) job_deps(w, g, tid, nthr);
+      break;
     default: break;
   }
 }
