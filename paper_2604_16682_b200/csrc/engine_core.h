@@ -2269,8 +2269,11 @@ EC_DEV SKey skey_of(const W* w, int j, int n_all) {
     k.k2 = 0xff00000000000000ull | (unsigned long long)j;
     return k;
   }
+  /* record index in the low 11 bits (RCAP <= 2048), push seq + 1 above it
+   * (< 2^45), the priority on top */
+  static_assert(W::RC <= 2048, "sort key holds an 11-bit record index");
   k.k1 = ec_bits(r.t);
-  k.k2 = ((unsigned long long)(unsigned)r.prio << 56) | ((unsigned long long)(r.seq + 1) << 8) |
+  k.k2 = ((unsigned long long)(unsigned)r.prio << 56) | ((unsigned long long)(r.seq + 1) << 11) |
          (unsigned long long)j;
   return k;
 }

@@ -188,3 +188,21 @@ def test_run_sharded_single_rank(cuda_device):
     assert res.totals["ticks"] == float(ctr[:, _abi.CTR["ticks"]].sum())
     assert res.totals["completed"] == float(ctr[:, _abi.CTR["completed"]].sum())
     assert len(res.local_results) == len(cfgs)
+
+
+@pytest.mark.parametrize("team", ["big", "quad"], indirect=True)
+def test_large_tie_storm_batches(cuda_device, team):
+    """Hundreds of identical agents: batches of several hundred records with
+    exact (time, priority) ties ordered by push sequence, past the 256th
+    record of the big team's 1,024-record buffer."""
+    base = asb.generate_workload(asb.WorkloadSpec(arrival_rate=0.5, duration=20.0, seed=5))[0]
+    cfgs = []
+    for n, inst, pol in ((600, 4, "round_robin"), (400, 2, "context_aware"), (700, 8, "least_loaded")):
+        traces = [asb.AgentTrace(f"r{i:04d}", base.arrival_time, base.turns[:12]) for i in range(n)]
+        cfgs.append(config_from_dict(asb, {"instances": inst, "capacity": 2_000_000, "duration": 300.0,
+                                           "router": {"policy": pol, "reassign_interval": 3}}, traces))
+    batch = prepare_batch(cfgs)
+    got, gst = gpu(batch)
+    want, wst = run_oracle(batch)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
