@@ -45,6 +45,12 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+def _tmp(target: str) -> str:
+    """Per-process temporary output: concurrent builds (one per rank under
+    torchrun) never write the same file; the final rename is atomic."""
+    return f"{target}.{os.getpid()}.tmp"
+
+
 def _run(cmd: list[str]) -> None:
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -61,7 +67,7 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
         PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
-        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", target + ".tmp", *srcs]
+        cmd = [_nvcc(), *NVCC_FLAGS, "-shared", "-o", _tmp(target), *srcs]
         if profile == "debug":
             cmd.insert(1, "-DASB_DEBUG_TRACE")
         elif profile:
@@ -73,7 +79,7 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)
-        os.replace(target + ".tmp", target)
+        os.replace(_tmp(target), target)
     return target
 
 
@@ -82,8 +88,8 @@ def build_trace_io(force: bool = False) -> str:
     src = os.path.join(CSRC, "trace_io.cpp")
     if force or _stale(TRACE_IO_LIB, [src]):
         os.makedirs(LIB_DIR, exist_ok=True)
-        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", TRACE_IO_LIB + ".tmp", src])
-        os.replace(TRACE_IO_LIB + ".tmp", TRACE_IO_LIB)
+        _run(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-o", _tmp(TRACE_IO_LIB), src])
+        os.replace(_tmp(TRACE_IO_LIB), TRACE_IO_LIB)
     return TRACE_IO_LIB
 
 
@@ -93,8 +99,8 @@ def build_oracle(force: bool = False) -> str:
     if force or _stale(ORACLE_LIB, deps):
         os.makedirs(os.path.dirname(ORACLE_LIB), exist_ok=True)
         _run(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-              "-o", ORACLE_LIB + ".tmp", src, "-lm"])
-        os.replace(ORACLE_LIB + ".tmp", ORACLE_LIB)
+              "-o", _tmp(ORACLE_LIB), src, "-lm"])
+        os.replace(_tmp(ORACLE_LIB), ORACLE_LIB)
     return ORACLE_LIB
 
 
@@ -104,8 +110,8 @@ def build_host_engine(force: bool = False) -> str:
     if force or _stale(HOST_ENGINE_LIB, deps):
         os.makedirs(os.path.dirname(HOST_ENGINE_LIB), exist_ok=True)
         _run(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
-              "-o", HOST_ENGINE_LIB + ".tmp", src])
-        os.replace(HOST_ENGINE_LIB + ".tmp", HOST_ENGINE_LIB)
+              "-o", _tmp(HOST_ENGINE_LIB), src])
+        os.replace(_tmp(HOST_ENGINE_LIB), HOST_ENGINE_LIB)
     return HOST_ENGINE_LIB
 
 
