@@ -170,8 +170,19 @@ EC_DEV void stk_f64(double* p, double v) {
 EC_DEV void stk_i32(int* p, int v) {
   asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(l2_keep()) : "memory");
 }
+/* two consecutive slots in one 16-byte (f64) / 8-byte (i32) load */
+EC_DEV void ldk_f64x2(const double* p, double& a, double& b) {
+  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(a), "=d"(b) : "l"(p), "l"(l2_keep()));
+}
+EC_DEV void ldk_i32x2(const int* p, int& a, int& b) {
+  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
+               : "=r"(a), "=r"(b) : "l"(p), "l"(l2_keep()));
+}
 #define EC_LDK_F64(p) ldk_f64(p)
 #define EC_LDK_I32(p) ldk_i32(p)
+#define EC_LDK_F64X2(p, a, b) ldk_f64x2((p), (a), (b))
+#define EC_LDK_I32X2(p, a, b) ldk_i32x2((p), (a), (b))
 #define EC_STK_F64(p, v) stk_f64((p), (v))
 #define EC_STK_I32(p, v) stk_i32((p), (v))
 #endif
