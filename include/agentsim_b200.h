@@ -208,7 +208,8 @@ typedef struct AsbOutputs {
    * of the optimistic batches: same results, far slower; meant for single
    * runs that need the series.  A capacity of
    *   n_instances * (2 + n_samples + n_epochs) + n_agents + 3 * n_turns
-   * can never overflow (one row per handler, engine.py:488-603). */
+   * can never overflow (one row per handler, engine.py:488-603).
+   * timeseries != NULL requires ts_off and ts_count (else ASB_ERR_ARG). */
   const int64_t* ts_off;
   AsbTimeseriesRow* timeseries;
   int64_t* ts_count;

@@ -405,6 +405,7 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
                       AsbTablePool tables, AsbOutputs out, int64_t total_agents, int64_t total_ring_slots,
                       void* d_workspace, size_t workspace_bytes, void* stream) {
   if (n_scen < 0 || max_instances < 1 || max_instances > 64) return ASB_ERR_ARG;
+  if (out.timeseries && (!out.ts_off || !out.ts_count)) return ASB_ERR_ARG; /* rows need their offsets and counts */
   if (n_scen == 0) return ASB_OK;
   size_t need = carve(nullptr, n_scen, total_agents, total_ring_slots, nullptr);
   if (!d_workspace || workspace_bytes < need) return ASB_ERR_WORKSPACE;

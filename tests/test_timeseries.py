@@ -153,3 +153,20 @@ def test_gpu_timeseries_batch_matches_oracle(cuda_device, seed, team):
     diff = array_outputs_equal(want, got, keys=[k for k in want if k not in (
         "agent_off", "inst_off", "dec_off", "turn_off", "ts_off", "timeseries")])
     assert diff is None, diff
+
+
+@pytest.mark.gpu
+def test_gpu_rows_without_offsets_are_rejected(cuda_device):
+    """asb_run_scenarios returns ASB_ERR_ARG for a row buffer without its
+    offsets / counts (include/agentsim_b200.h), raised by the host mirror."""
+    import torch
+
+    from paper_2604_16682_b200 import ops
+    from paper_2604_16682_b200.engine import DeviceBatch
+
+    t, g, cfg = ts_config("ka_single_agent.json.gz")
+    dev = DeviceBatch(prepare_batch([cfg]), device="cuda:0", timeseries=True)
+    dev.outputs["ts_off"] = torch.empty(0, dtype=torch.int64, device="cuda:0")
+    dev.out_list = [dev.outputs[k] for k in ops.OUT_NAMES]
+    with pytest.raises(RuntimeError):
+        dev.run()
