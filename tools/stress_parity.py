@@ -2,7 +2,7 @@
 every team shape against the C oracle (bit-exact).  A kernel that fails to
 finish is caught by the host watchdog thread (exit code 3).
 
-    python tools/stress_parity.py [n_batches] [configs_per_batch]
+    python tools/stress_parity.py [n_batches] [configs_per_batch] [first_seed]
 
 Every 4th batch also runs in timeseries mode (rows compared byte for byte);
 every 3rd batch widens its scenarios to 17-64 instances (the MAXM=64
@@ -31,6 +31,7 @@ from test_host_engine import random_configs  # noqa: E402
 def main():
     n_batches = int(sys.argv[1]) if len(sys.argv) > 1 else 40
     per = int(sys.argv[2]) if len(sys.argv) > 2 else 48
+    seed0 = int(sys.argv[3]) if len(sys.argv) > 3 else 1000
     state = {"t": time.time(), "what": ""}
 
     def watchdog():
@@ -45,7 +46,7 @@ def main():
     for b in range(n_batches):
         team = ("solo", "quad", "big")[b % 3]
         os.environ["ASB_TEAM"] = team
-        seed = 1000 + b
+        seed = seed0 + b
         state["t"], state["what"] = time.time(), f"batch {b} seed {seed} team {team}"
         cfgs = random_configs(seed, per)
         wide = b % 3 == 2
