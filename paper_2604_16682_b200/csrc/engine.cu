@@ -55,6 +55,7 @@ EC_DEV unsigned t_lt_mask() {
 }
 EC_DEV int ec_popc(unsigned m) { return __popc(m); }
 EC_DEV int ec_ffs(unsigned m) { return __ffs(m); } /* 1-based lowest set bit, 0 if none */
+EC_DEV unsigned t_match_any_i(int v) { return __match_any_sync(FULLMASK, v); } /* lanes holding the same v */
 EC_DEV unsigned t_redux_min_u32(unsigned v) { return __reduce_min_sync(FULLMASK, v); }
 EC_DEV long long t_bcast_ll(long long v, int src) { return __shfl_sync(FULLMASK, v, src); }
 /* warp collectives used at many call sites: out of line and rolled to keep

@@ -45,7 +45,7 @@
 
 /* ---- team primitives: provided by the includer ----------------------------
  *   EC_DEV, EC_LANE, EC_TSIZE, t_sync(), t_ballot(p), t_lt_mask(), ec_popc,
- *   t_bcast_ll, t_scan_add_ll, t_sum_ll, t_shfl_xor_{ull,ll,i},
+ *   t_bcast_ll, t_scan_add_ll, t_sum_ll, t_shfl_xor_{ull,ll,i}, t_match_any_i,
  *   t_atomic_min_ull, t_atomic_add_i, ec_isnan, ec_floor, ec_bits,
  *   ec_from_bits, ec_clock, EC_NAN, EC_INF, EC_INF_BITS
  */
@@ -2211,10 +2211,62 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   t_sync();
   EC_WPROF(w, 4);
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
-  if (EC_WIDE_LANE_PAR && n_dep > 0 && M > EC_TSIZE) {
-    /* many instances: route every arrival in parallel (JOB_DEPS or a lane
-     * per arrival), commit in order */
-    if (!team_deps) route_parallel(w, n_dep, stop_p);
+  if (team_deps) {
+    /* many instances, routed by JOB_DEPS: commit the arrivals a lane each
+     * (_on_arrival bookkeeping, engine.py:490-507, as commit_arrival does
+     * it one by one): arrival rank, alive slot and arrival_rank from the
+     * lane's rank among the batch's arrivals, FIFO position from the earlier
+     * arrivals to the same instance */
+    int done = 0;
+    for (int base = 0; base < n_dep; base += EC_TSIZE) {
+      const int k = base + EC_LANE;
+      const int p = k < n_dep ? w->dep_pos[k] : 0x7fffffff;
+      const bool arr = p < stop_p && w->sw_prio[p] == EV_ARRIVAL;
+      const unsigned m = t_ballot(arr);
+      if (!m) continue;
+      const int rank = done + ec_popc(m & t_lt_mask());
+      int target = 0, a = -1, order_pos = 0;
+      if (arr) {
+        const Rec& r = w->rec[w->sw_idx[p]];
+        a = r.agent;
+        order_pos = (int)r.seq;
+        target = sc.policy == ASB_POLICY_ROUND_ROBIN ? (int)(((long long)w->rr_next + rank) % M) + 1
+                                                     : w->dep_target[k];
+      }
+      const unsigned peers = t_match_any_i(arr ? target : 0) & m;
+      const int same_before = ec_popc(peers & t_lt_mask());
+      if (arr) {
+        const Inst& dst = w->in[target - 1];
+        g.ring[(long long)(target - 1) * g.A + ring_idx(dst.fifo_head, dst.fifo_len + same_before, g.A)] = a;
+        g.H[a].inst = target;
+        g.H[a].sa = 0;
+        g.H[a].phase = ASB_PHASE_PENDING;
+        g.H[a].next_prio = 0;
+        const int j = w->n_alive + rank;
+        EC_STK_I32(&g.alive[j], a);
+        g.H[a].slot = j;
+        EC_STK_F64(&g.s_tp[j], EC_INF);
+        EC_STK_F64(&g.s_next[j], 0.0);
+        EC_STK_I32(&g.s_meta[j], target);
+        g.rank[a] = w->arr_rank + rank;
+      }
+      t_sync(); /* every lane has read fifo_len before the groups advance it */
+      if (arr && (peers >> EC_LANE) == 1u) w->in[target - 1].fifo_len += ec_popc(peers); /* last lane of its group */
+      if (arr && (m >> EC_LANE) == 1u) w->arr_ptr = order_pos + 1; /* the chunk's last arrival */
+      done += ec_popc(m);
+      t_sync();
+    }
+    EC_LANE0 {
+      w->n_alive += done;
+      w->arr_rank += done;
+      if (sc.policy == ASB_POLICY_ROUND_ROBIN) w->rr_next += done;
+      w->ctr[ASB_CTR_ARRIVED] += done;
+    }
+    t_sync();
+  } else if (EC_WIDE_LANE_PAR && n_dep > 0 && M > EC_TSIZE) {
+    /* many instances: route every arrival in parallel (a lane per arrival),
+     * commit in order */
+    route_parallel(w, n_dep, stop_p);
     EC_LANE0 {
       for (int k = 0; k < n_dep; k++) {
         const int p = w->dep_pos[k];

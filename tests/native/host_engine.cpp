@@ -25,6 +25,7 @@ static inline unsigned t_ballot(bool p) { return p ? 1u : 0u; }
 static inline unsigned t_lt_mask() { return 0u; }
 static inline int ec_popc(unsigned m) { return __builtin_popcount(m); }
 static inline int ec_ffs(unsigned m) { return __builtin_ffs((int)m); }
+static inline unsigned t_match_any_i(int) { return 1u; }
 static inline unsigned t_redux_min_u32(unsigned v) { return v; }
 static inline long long t_bcast_ll(long long v, int) { return v; }
 static inline long long t_scan_add_ll(long long v) { return v; }
