@@ -96,13 +96,14 @@ EC_DEV long long ec_clock() { return clock64(); }
 /* named CTA barriers for the fork-join team.  Each warp reconverges first
  * (__syncwarp): a warp that reaches a CTA barrier with some lanes still
  * inside the job would let the barrier complete early. */
+/* a single-warp team is its own team: a warp barrier is enough */
 EC_DEV void ec_fork_begin(int nt) {
   __syncwarp();
-  asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+  if (nt > 32) asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
 }
 EC_DEV void ec_fork_end(int nt) {
   __syncwarp();
-  asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
+  if (nt > 32) asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
 }
 EC_DEV void ec_team_barrier() {
   __syncwarp();
