@@ -375,7 +375,11 @@ def main():
     peak, peak_src = hbm_peak()
     traffic, _ = ncu_traffic(args.config)
 
-    # end-to-end through the public API with host buffers (pinned H2D + D2H of results)
+    # end-to-end through the public API with host buffers: every step copies
+    # its inputs from pinned host memory and reads its results back.  Two
+    # device input sets and a copy stream pipeline the steps: step k+1's
+    # inputs upload while step k computes (each step still waits for its own
+    # upload, and an input set is only overwritten after the step using it)
     e2e = None
     if not args.no_e2e:
         host_in = [torch.from_numpy(np.ascontiguousarray(batch.scen.view(np.uint8))).pin_memory()]
@@ -383,22 +387,51 @@ def main():
                     for k in _abi.TRACE_FIELDS]
         host_in += [torch.from_numpy(np.ascontiguousarray(getattr(batch.tables, k))).pin_memory()
                     for k in _abi.TABLE_FIELDS]
-        dev_in = [db.scen, *db.traces, *db.tables]
+        sets = [[db.scen, *db.traces, *db.tables],
+                [torch.empty(t.shape, dtype=t.dtype, device=dev) for t in host_in]]
+        nt, ntab = len(_abi.TRACE_FIELDS), len(_abi.TABLE_FIELDS)
         h2d = sum(t.numel() * t.element_size() for t in host_in)
         out_stats = torch.empty(db.stats.shape, dtype=db.stats.dtype).pin_memory()
         out_red = torch.empty(db.red.shape, dtype=db.red.dtype).pin_memory()
         d2h = out_stats.numel() + out_red.numel() * 8
+        copy_stream = torch.cuda.Stream(dev)
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        used = [torch.cuda.Event(), torch.cuda.Event()]
+
+        def upload(k):
+            dst = sets[k % 2]
+            with torch.cuda.stream(copy_stream):
+                if k >= 2:
+                    copy_stream.wait_event(used[k % 2])  # step k-2 is done with this set
+                for d_t, h_t in zip(dst, host_in):
+                    d_t.copy_(h_t, non_blocking=True)
+                copied[k % 2].record(copy_stream)
+
+        def step_on(k):
+            inp = sets[k % 2]
+            scen, traces, tables = inp[0], inp[1:1 + nt], inp[1 + nt:1 + nt + ntab]
+            stream.wait_event(copied[k % 2])
+            torch.ops.agentsim_b200.run_scenarios(scen, traces, tables, db.out_list, db.workspace,
+                                                  batch.max_instances, batch.total_agents, batch.total_ring)
+            torch.ops.agentsim_b200.scenario_stats(scen, db.out_list, db.stats)
+            used[k % 2].record(stream)
+            torch.ops.agentsim_b200.reduce_stats(db.stats, db.outputs["counters"], batch.n, db.red)
+            if pg is not None:
+                allreduce_stats(db.red)
+            out_stats.copy_(db.stats, non_blocking=True)
+            out_red.copy_(db.red, non_blocking=True)
+
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         if pg is not None:
             pg.barrier()
         e0.record(stream)
-        for _ in range(args.steps):
-            for d_t, h_t in zip(dev_in, host_in):
-                d_t.copy_(h_t, non_blocking=True)
-            step()
-            out_stats.copy_(db.stats, non_blocking=True)
-            out_red.copy_(db.red, non_blocking=True)
+        copy_stream.wait_event(e0)
+        upload(0)
+        for k in range(args.steps):
+            if k + 1 < args.steps:
+                upload(k + 1)
+            step_on(k)
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = e0.elapsed_time(e1) / args.steps
@@ -407,7 +440,8 @@ def main():
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             e2e_ms = float(t[0])
         e2e = {"value": ticks_all / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms,
+               "pipelining": "two device input sets: step k+1's upload overlaps step k's compute"}
 
     cpu = None
     parity = None
