@@ -207,8 +207,12 @@ typedef struct AsbOutputs {
    * serial event loop (one event at a time, sample events included) instead
    * of the optimistic batches: same results, far slower; meant for single
    * runs that need the series.  A capacity of
-   *   n_instances * (2 + n_samples + n_epochs) + n_agents + 3 * n_turns
-   * can never overflow (one row per handler, engine.py:488-603).
+   *   n_instances * (2 + n_samples + n_epochs) + n_agents + n_turns
+   *     + 3 * (n_turns - n_agents)
+   * can never overflow: forced rows per instance (engine.py:488, 572, 579,
+   * 603), one per arrival and completion (507, 535), two per tool event
+   * (source and migration target, 549, 560-561) and one per delayed start,
+   * which only follows a migration (568).
    * timeseries != NULL requires ts_off and ts_count (else ASB_ERR_ARG). */
   const int64_t* ts_off;
   AsbTimeseriesRow* timeseries;
@@ -251,7 +255,7 @@ int asb_scenario_stats(const AsbScenario* d_scen, int32_t n_scen, AsbOutputs out
                        void* stream);
 
 /* Batched unit ops (SPEC acceptance criteria 1-2 grids; K3/K4 of SURVEY §2). */
-int asb_select_level_batch(const int64_t* usage, const int64_t* capacity,
+int asb_select_level_batch(const double* usage, const double* capacity,
                            const int32_t* num_levels, const double* alpha, int32_t* level_out,
                            int64_t n, void* stream);
 int asb_service_time_batch(const int32_t* prefill, const int32_t* decode,

@@ -14,17 +14,25 @@
  * would reject — is reported with its line number and the Python loader
  * (the reference's exact semantics and error messages) handles the file.
  *
- * Numbers are parsed with std::from_chars, correctly rounded like Python's
- * float(); token counts must be integral and fit in int32 (the engine's
- * layout).  Two passes: a sizing pass, then a fill pass into caller buffers.
+ * Numbers must follow the JSON grammar exactly (RFC 8259 §6: optional '-',
+ * no leading zeros, digits on both sides of '.', digits after the exponent;
+ * json.loads rejects "1.", ".5", "0400", "+1") and are then converted with
+ * std::from_chars, correctly rounded like Python's float(); token counts
+ * must be integral and fit in int32 (the engine's layout).
+ *
+ * The file is read ONCE into a parsed handle; the caller sizes its buffers
+ * from the handle's counts and copies out of it, so a file that changes
+ * between the two calls cannot overrun anything.
  *
  * C ABI (ctypes, paper_2604_16682_b200/workload.py):
- *   int asb_trace_scan(const char* path, int64_t* n_agents, int64_t* n_turns,
- *                      int64_t* id_bytes, int64_t* bad_line);
- *   int asb_trace_fill(const char* path, double* arrival, int64_t* turn_off,
+ *   int asb_trace_parse(const char* path, void** handle, int64_t* n_agents,
+ *                       int64_t* n_turns, int64_t* id_bytes, int64_t* bad_line);
+ *   int asb_trace_copy(const void* handle, double* arrival, int64_t* turn_off,
  *                      int32_t* prefill, int32_t* decode, double* tool,
- *                      char* ids, int64_t* id_off, int64_t* bad_line);
- * return 0 ok, 1 = needs the Python loader (bad_line = 1-based line), -1 I/O.
+ *                      char* ids, int64_t* id_off);
+ *   void asb_trace_free(void* handle);
+ * parse returns 0 ok (handle set), 1 = needs the Python loader (bad_line =
+ * 1-based line), -1 I/O; copy returns 0 (or -1 for a NULL handle).
  */
 #include <errno.h>
 #include <math.h>
@@ -91,20 +99,41 @@ bool parse_string(Cursor& c, std::string* out) {
   return true;
 }
 
+/* JSON number (RFC 8259 §6): -? (0 | [1-9][0-9]*) (. [0-9]+)? ([eE] [+-]? [0-9]+)? */
+const char* json_number_end(const char* s, const char* end) {
+  if (s < end && *s == '-') s++;
+  if (s >= end || *s < '0' || *s > '9') return nullptr;
+  if (*s == '0') {
+    s++;
+  } else {
+    while (s < end && *s >= '0' && *s <= '9') s++;
+  }
+  if (s < end && *s == '.') {
+    s++;
+    if (s >= end || *s < '0' || *s > '9') return nullptr;
+    while (s < end && *s >= '0' && *s <= '9') s++;
+  }
+  if (s < end && (*s == 'e' || *s == 'E')) {
+    s++;
+    if (s < end && (*s == '+' || *s == '-')) s++;
+    if (s >= end || *s < '0' || *s > '9') return nullptr;
+    while (s < end && *s >= '0' && *s <= '9') s++;
+  }
+  /* "0400" parses as "0" followed by "400": the next token check rejects it */
+  if (s < end && ((*s >= '0' && *s <= '9') || *s == '.' || *s == 'e' || *s == 'E' || *s == '+' || *s == '-'))
+    return nullptr;
+  return s;
+}
+
 bool parse_number(Cursor& c, double* v, bool* integral) {
   c.ws();
-  const char* s = c.p;
-  if (s < c.end && (*s == '-' || *s == '+')) s++;
-  bool dig = false, frac = false;
-  while (s < c.end && ((*s >= '0' && *s <= '9') || *s == '.' || *s == 'e' || *s == 'E' || *s == '-' || *s == '+')) {
-    if (*s >= '0' && *s <= '9') dig = true;
-    if (*s == '.' || *s == 'e' || *s == 'E') frac = true;
-    s++;
-  }
-  if (!dig) return false;
-  /* correctly rounded (like Python's float()); a leading '+' is not JSON */
+  const char* s = json_number_end(c.p, c.end);
+  if (!s) return false;
+  bool frac = false;
+  for (const char* q = c.p; q < s; q++)
+    if (*q == '.' || *q == 'e' || *q == 'E') frac = true;
+  /* correctly rounded (like Python's float()) */
   double x = 0.0;
-  if (*c.p == '+') return false;
   const std::from_chars_result r = std::from_chars(c.p, s, x);
   if (r.ptr != s || r.ec != std::errc() || !isfinite(x)) return false;
   if (!frac && x == 0) x = 0.0; /* "-0" is the int 0 in json.loads, float(0) == +0.0 */
@@ -262,42 +291,60 @@ int walk(const char* path, int64_t* bad_line, Fn fn) {
   return 0;
 }
 
+/* the whole file, parsed once */
+struct Parsed {
+  std::vector<double> arrival, tool;
+  std::vector<int64_t> turn_off, id_off;
+  std::vector<int32_t> pre, dec;
+  std::string ids;
+};
+
 }  // namespace
 
 extern "C" {
 
-int asb_trace_scan(const char* path, int64_t* n_agents, int64_t* n_turns, int64_t* id_bytes, int64_t* bad_line) {
-  int64_t na = 0, nt = 0, nb = 0;
+int asb_trace_parse(const char* path, void** handle, int64_t* n_agents, int64_t* n_turns, int64_t* id_bytes,
+                    int64_t* bad_line) {
+  *handle = nullptr;
   *bad_line = 0;
-  int rc = walk(path, bad_line, [&](int64_t, const Agent& a) {
-    na++;
-    nt += (int64_t)a.pre.size();
-    nb += (int64_t)a.id.size();
+  Parsed* P = new Parsed();
+  P->turn_off.push_back(0);
+  P->id_off.push_back(0);
+  const int rc = walk(path, bad_line, [&](int64_t, const Agent& a) {
+    P->arrival.push_back(a.arrival);
+    P->pre.insert(P->pre.end(), a.pre.begin(), a.pre.end());
+    P->dec.insert(P->dec.end(), a.dec.begin(), a.dec.end());
+    P->tool.insert(P->tool.end(), a.tool.begin(), a.tool.end());
+    P->turn_off.push_back((int64_t)P->pre.size());
+    P->ids += a.id;
+    P->id_off.push_back((int64_t)P->ids.size());
   });
-  *n_agents = na;
-  *n_turns = nt;
-  *id_bytes = nb;
-  return rc;
+  if (rc != 0) {
+    delete P;
+    return rc;
+  }
+  *n_agents = (int64_t)P->arrival.size();
+  *n_turns = (int64_t)P->pre.size();
+  *id_bytes = (int64_t)P->ids.size();
+  *handle = P;
+  return 0;
 }
 
-int asb_trace_fill(const char* path, double* arrival, int64_t* turn_off, int32_t* prefill, int32_t* decode,
-                   double* tool, char* ids, int64_t* id_off, int64_t* bad_line) {
-  int64_t t = 0, ib = 0;
-  *bad_line = 0;
-  turn_off[0] = 0;
-  id_off[0] = 0;
-  return walk(path, bad_line, [&](int64_t i, const Agent& a) {
-    arrival[i] = a.arrival;
-    const size_t n = a.pre.size();
-    memcpy(prefill + t, a.pre.data(), n * 4);
-    memcpy(decode + t, a.dec.data(), n * 4);
-    memcpy(tool + t, a.tool.data(), n * 8);
-    t += (int64_t)n;
-    turn_off[i + 1] = t;
-    memcpy(ids + ib, a.id.data(), a.id.size());
-    ib += (int64_t)a.id.size();
-    id_off[i + 1] = ib;
-  });
+int asb_trace_copy(const void* handle, double* arrival, int64_t* turn_off, int32_t* prefill, int32_t* decode,
+                   double* tool, char* ids, int64_t* id_off) {
+  const Parsed* P = static_cast<const Parsed*>(handle);
+  if (!P) return -1;
+  const size_t na = P->arrival.size(), nt = P->pre.size();
+  memcpy(arrival, P->arrival.data(), na * 8);
+  memcpy(turn_off, P->turn_off.data(), (na + 1) * 8);
+  memcpy(prefill, P->pre.data(), nt * 4);
+  memcpy(decode, P->dec.data(), nt * 4);
+  memcpy(tool, P->tool.data(), nt * 8);
+  memcpy(ids, P->ids.data(), P->ids.size());
+  memcpy(id_off, P->id_off.data(), (na + 1) * 8);
+  return 0;
 }
+
+void asb_trace_free(void* handle) { delete static_cast<Parsed*>(handle); }
 
 }  // extern "C"

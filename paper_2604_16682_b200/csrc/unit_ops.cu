@@ -33,13 +33,14 @@ inline int grid_for(int64_t n, int threads) {
   return (int)(b < 1 ? 1 : b);
 }
 
-__global__ void select_level_kernel(const int64_t* __restrict__ usage, const int64_t* __restrict__ capacity,
+__global__ void select_level_kernel(const double* __restrict__ usage, const double* __restrict__ capacity,
                                     const int32_t* __restrict__ num_levels, const double* __restrict__ alpha,
                                     int32_t* __restrict__ out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    double ac = alpha[i] * (double)capacity[i];
+    /* usage and capacity are floats in the reference's signature */
+    double ac = alpha[i] * capacity[i];
     int L = num_levels[i];
-    double u = (double)usage[i];
+    double u = usage[i];
     out[i] = u >= ac ? L : (int)floor(u / ac * (double)(L - 1)) + 1;
   }
 }
@@ -298,7 +299,7 @@ __global__ void reduce_stats_kernel(const AsbStats* __restrict__ stats, const in
 
 extern "C" {
 
-int asb_select_level_batch(const int64_t* usage, const int64_t* capacity, const int32_t* num_levels,
+int asb_select_level_batch(const double* usage, const double* capacity, const int32_t* num_levels,
                            const double* alpha, int32_t* level_out, int64_t n, void* stream) {
   if (n < 0) return ASB_ERR_ARG;
   if (n == 0) return ASB_OK;

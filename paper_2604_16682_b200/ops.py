@@ -42,6 +42,13 @@ def _stream(t: torch.Tensor) -> int:
     return _native.stream_handle(t.device)
 
 
+def _on(t: torch.Tensor):
+    """The C ABI launches on the CURRENT device (cudaGetDevice, kernel
+    attributes, the launch itself): make it the tensors' device, so that
+    ``device='cuda:1'`` with cuda:0 current gets cuda:1's stream and memory."""
+    return torch.cuda.device(t.device)
+
+
 # --------------------------------------------------------------------------- engine
 
 
@@ -64,8 +71,9 @@ def run_scenarios(
     tb = _abi.make_pool(_abi.AsbTablePool, _ptr, dict(zip(_abi.TABLE_FIELDS, tables)), "n_tables",
                         tables[0].numel() - 1)
     out = _abi.make_outputs(_ptr, dict(zip(OUT_NAMES, outputs)))
-    rc = lib.asb_run_scenarios(_ptr(scen), n_scen, max_instances, tp, tb, out, total_agents, total_ring,
-                               _ptr(workspace), workspace.numel(), _stream(scen))
+    with _on(scen):
+        rc = lib.asb_run_scenarios(_ptr(scen), n_scen, max_instances, tp, tb, out, total_agents, total_ring,
+                                   _ptr(workspace), workspace.numel(), _stream(scen))
     _native.check(rc, "asb_run_scenarios")
 
 
@@ -75,13 +83,15 @@ def scenario_stats(scen: torch.Tensor, outputs: list[torch.Tensor], stats: torch
     lib = _native.lib()
     n_scen = scen.numel() // _abi.SCENARIO_DTYPE.itemsize
     out = _abi.make_outputs(_ptr, dict(zip(OUT_NAMES, outputs)))
-    rc = lib.asb_scenario_stats(_ptr(scen), n_scen, out, _ptr(stats), None, 0, _stream(scen))
+    with _on(scen):
+        rc = lib.asb_scenario_stats(_ptr(scen), n_scen, out, _ptr(stats), None, 0, _stream(scen))
     _native.check(rc, "asb_scenario_stats")
 
 
 @torch.library.custom_op(f"{_NS}::reduce_stats", mutates_args=("red",))
 def reduce_stats(stats: torch.Tensor, counters: torch.Tensor, n_scen: int, red: torch.Tensor) -> None:
-    rc = _native.lib().asb_reduce_stats(_ptr(stats), _ptr(counters), n_scen, _ptr(red), _stream(red))
+    with _on(red):
+        rc = _native.lib().asb_reduce_stats(_ptr(stats), _ptr(counters), n_scen, _ptr(red), _stream(red))
     _native.check(rc, "asb_reduce_stats")
 
 
@@ -92,8 +102,9 @@ def reduce_stats(stats: torch.Tensor, counters: torch.Tensor, n_scen: int, red: 
 def select_frequency_level(usage: torch.Tensor, capacity: torch.Tensor, num_levels: torch.Tensor,
                            alpha: torch.Tensor) -> torch.Tensor:
     out = torch.empty(usage.shape, dtype=torch.int32, device=usage.device)
-    rc = _native.lib().asb_select_level_batch(_ptr(usage), _ptr(capacity), _ptr(num_levels), _ptr(alpha),
-                                              _ptr(out), usage.numel(), _stream(usage))
+    with _on(usage):
+        rc = _native.lib().asb_select_level_batch(_ptr(usage), _ptr(capacity), _ptr(num_levels), _ptr(alpha),
+                                                  _ptr(out), usage.numel(), _stream(usage))
     _native.check(rc, "asb_select_level_batch")
     return out
 
@@ -108,9 +119,10 @@ def service_time(prefill: torch.Tensor, decode: torch.Tensor, prefill_rate: torc
                  decode_rate: torch.Tensor, concurrent: torch.Tensor, thrashing: torch.Tensor,
                  interference: float, thrash_factor: float) -> torch.Tensor:
     out = torch.empty(prefill.shape, dtype=torch.float64, device=prefill.device)
-    rc = _native.lib().asb_service_time_batch(_ptr(prefill), _ptr(decode), _ptr(prefill_rate), _ptr(decode_rate),
-                                              _ptr(concurrent), _ptr(thrashing), interference, thrash_factor,
-                                              _ptr(out), prefill.numel(), _stream(prefill))
+    with _on(prefill):
+        rc = _native.lib().asb_service_time_batch(_ptr(prefill), _ptr(decode), _ptr(prefill_rate), _ptr(decode_rate),
+                                                  _ptr(concurrent), _ptr(thrashing), interference, thrash_factor,
+                                                  _ptr(out), prefill.numel(), _stream(prefill))
     _native.check(rc, "asb_service_time_batch")
     return out
 
@@ -123,8 +135,9 @@ def _(prefill, decode, prefill_rate, decode_rate, concurrent, thrashing, interfe
 @torch.library.custom_op(f"{_NS}::route_assign", mutates_args=())
 def route_assign(usages: torch.Tensor, m: torch.Tensor, capacity: int, threshold: float, policy: int) -> torch.Tensor:
     out = torch.empty(usages.shape[0], dtype=torch.int32, device=usages.device)
-    rc = _native.lib().asb_assign_batch(_ptr(usages), _ptr(m), usages.shape[1], capacity, threshold, policy,
-                                        _ptr(out), usages.shape[0], _stream(usages))
+    with _on(usages):
+        rc = _native.lib().asb_assign_batch(_ptr(usages), _ptr(m), usages.shape[1], capacity, threshold, policy,
+                                            _ptr(out), usages.shape[0], _stream(usages))
     _native.check(rc, "asb_assign_batch")
     return out
 
@@ -138,9 +151,10 @@ def _(usages, m, capacity, threshold, policy):
 def route_reassign(usages: torch.Tensor, m: torch.Tensor, current: torch.Tensor, counters: torch.Tensor,
                    interval: int, ratio: float, include_idle: bool, reset_only: bool) -> torch.Tensor:
     out = torch.empty(usages.shape[0], dtype=torch.int32, device=usages.device)
-    rc = _native.lib().asb_reassign_batch(_ptr(usages), _ptr(m), usages.shape[1], _ptr(current), _ptr(counters),
-                                          interval, ratio, int(include_idle), int(reset_only), _ptr(out),
-                                          usages.shape[0], _stream(usages))
+    with _on(usages):
+        rc = _native.lib().asb_reassign_batch(_ptr(usages), _ptr(m), usages.shape[1], _ptr(current), _ptr(counters),
+                                              interval, ratio, int(include_idle), int(reset_only), _ptr(out),
+                                              usages.shape[0], _stream(usages))
     _native.check(rc, "asb_reassign_batch")
     return out
 
@@ -150,9 +164,10 @@ def min_throughput(decode_total: torch.Tensor, llm_time: torch.Tensor, segment: 
                    n_seg: int) -> torch.Tensor:
     out = torch.empty(n_seg, dtype=torch.float64, device=decode_total.device)
     scratch = torch.empty(n_seg, dtype=torch.float64, device=decode_total.device)
-    rc = _native.lib().asb_min_throughput_batch(_ptr(decode_total), _ptr(llm_time), _ptr(segment),
-                                                decode_total.numel(), n_seg, _ptr(scratch), _ptr(out),
-                                                _stream(decode_total))
+    with _on(decode_total):
+        rc = _native.lib().asb_min_throughput_batch(_ptr(decode_total), _ptr(llm_time), _ptr(segment),
+                                                    decode_total.numel(), n_seg, _ptr(scratch), _ptr(out),
+                                                    _stream(decode_total))
     _native.check(rc, "asb_min_throughput_batch")
     return out
 
@@ -167,8 +182,8 @@ def _dev(device=None):
 def select_level_batch(usage, capacity, num_levels, alpha, device=None) -> np.ndarray:
     d = _dev(device)
     out = torch.ops.agentsim_b200.select_frequency_level(
-        torch.as_tensor(np.asarray(usage, dtype=np.int64), device=d),
-        torch.as_tensor(np.asarray(capacity, dtype=np.int64), device=d),
+        torch.as_tensor(np.asarray(usage, dtype=np.float64), device=d),
+        torch.as_tensor(np.asarray(capacity, dtype=np.float64), device=d),
         torch.as_tensor(np.asarray(num_levels, dtype=np.int32), device=d),
         torch.as_tensor(np.asarray(alpha, dtype=np.float64), device=d),
     )

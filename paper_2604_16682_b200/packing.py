@@ -209,14 +209,22 @@ def sample_count(sim_duration: float, record_interval: float) -> int:
 
 
 def timeseries_capacity(scen: np.ndarray, a_cnt: np.ndarray, t_cnt: np.ndarray) -> np.ndarray:
-    """Per-scenario row bound that _mark_row can never exceed: one row per
-    instance at start, end, every sample and every epoch (engine.py:488, 572,
-    579, 603) plus at most one per arrival, per completion, per tool event and
-    per delayed start (each <= turns; engine.py:507, 535, 549/561, 568)."""
+    """Per-scenario row bound that _mark_row can never exceed.
+
+    * one row per instance at start, end, every sample and every epoch
+      (engine.py:488, 572, 579, 603);
+    * one per arrival (engine.py:507) and one per completion (engine.py:535);
+    * a tool event (at most T - A of them: the last turn has none) marks its
+      source and, when it migrates, its target (engine.py:549, 560-561);
+    * a delayed start (engine.py:568) follows only a migration, so at most
+      one per tool event.
+
+    Every agent has at least one turn (workload.py:114-115), so T >= A."""
     m = scen["n_instances"].astype(np.int64)
     samples = np.array([sample_count(float(r["sim_duration"]), float(r["record_interval"])) for r in scen],
                        dtype=np.int64).reshape(-1)
-    return m * (2 + samples + scen["n_epochs"].astype(np.int64)) + a_cnt + 3 * t_cnt
+    tools = np.maximum(t_cnt - a_cnt, 0)
+    return m * (2 + samples + scen["n_epochs"].astype(np.int64)) + a_cnt + t_cnt + 3 * tools
 
 
 @dataclass

@@ -46,14 +46,52 @@ def scenario_weights(batch) -> np.ndarray:
 
 
 def config_weights(configs) -> np.ndarray:
-    """Σ trace turns per SimConfig (configs with resolved ``traces``)."""
+    """LPT cost proxy per SimConfig without packing anything (every rank
+    computes it identically from the configs alone): Σ trace turns for
+    inline traces, the expected turn count (arrival_rate · duration · mean
+    turns, workload.py:134-152) for a WorkloadSpec, the file size for a
+    trace path."""
+    import os
+
+    from .engine import _trace_key
+
     out = np.zeros(len(configs), dtype=np.int64)
+    memo: dict = {}
     for s, c in enumerate(configs):
-        if c.traces is not None:
-            out[s] = sum(len(t.turns) for t in c.traces)
-        else:
-            out[s] = 1
+        key = _trace_key(c)
+        if key not in memo:
+            if key[0] == "objects":
+                w = sum(len(t.turns) for t in c.traces)
+            elif key[0] == "path":
+                w = os.path.getsize(c.trace_path) // 64 if os.path.exists(c.trace_path) else 1
+            else:
+                spec = key[1]
+                w = int(spec.arrival_rate * spec.duration * spec.turn_count.mean)
+            memo[key] = max(int(w), 1)
+        out[s] = memo[key]
     return out
+
+
+def check_status_all(counters, group=None) -> None:
+    """Raise SimulationError on EVERY rank when any scenario on any rank
+    reported a device status (overflow, livelock, invariant violation): one
+    all_reduce(MAX) of the local worst status, so no rank returns partial
+    aggregates."""
+    import torch
+    import torch.distributed as dist
+
+    from .errors import SimulationError
+
+    ctr = counters.view(-1, _abi.ASB_NCOUNTERS) if counters.numel() else counters.view(0, _abi.ASB_NCOUNTERS)
+    st = ctr[:, _abi.CTR["status"]]
+    worst = torch.zeros(1, dtype=torch.int64, device=counters.device)
+    if st.numel():
+        worst = torch.maximum(worst, st.max().reshape(1))
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(worst, op=dist.ReduceOp.MAX, group=group)
+    code = int(worst.item())
+    if code:
+        raise SimulationError(f"a scenario of the sharded run reported {_abi.SIMERR.get(code, code)}")
 
 
 def partition_lpt(weights: Sequence[int] | np.ndarray, world: int) -> list[np.ndarray]:
@@ -143,7 +181,8 @@ def run_sharded(configs, *, group=None, device=None, results: bool = False, gath
     """Run a list of SimConfigs sharded over the ranks of ``group``.
 
     Each rank takes its LPT share, runs it on its GPU (one persistent engine
-    launch), folds the stats on device and joins one all_reduce; with
+    launch), folds the stats on device and joins one all_reduce; a device
+    status on any rank raises SimulationError on every rank; with
     ``gather`` the per-scenario SystemMetrics rows are all-gathered into
     global order.  There is no CPU fallback.
     """
@@ -158,9 +197,8 @@ def run_sharded(configs, *, group=None, device=None, results: bool = False, gath
     dev = _native.device(device)
     for c in configs:
         c.validate()
-    # weights from the resolved traces: pack everything once per rank (host work)
-    full = prepare_batch(configs)
-    owned = partition_lpt(scenario_weights(full), world)[rank]
+    # weights from the configs alone: no rank packs scenarios it does not run
+    owned = partition_lpt(config_weights(configs), world)[rank]
     mine = [configs[int(s)] for s in owned]
     local_res: list = []
     if mine:
@@ -174,6 +212,7 @@ def run_sharded(configs, *, group=None, device=None, results: bool = False, gath
         red = torch.zeros(_abi.ASB_NRED, dtype=torch.float64, device=dev)
         stats_rows = torch.empty(0, dtype=torch.uint8, device=dev)
         ctr = torch.empty(0, dtype=torch.int64, device=dev)
+    check_status_all(ctr, group)
     red = allreduce_stats(red.clone(), group)
     all_stats = np.zeros(0, dtype=_abi.STATS_DTYPE)
     all_ctr = np.zeros((0, _abi.ASB_NCOUNTERS), dtype=np.int64)

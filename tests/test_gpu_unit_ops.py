@@ -27,6 +27,21 @@ def test_ac1_frequency_formula_grid(cuda_device):
             assert (np.diff(got) >= 0).all() and got.min() >= 1 and got.max() <= L
 
 
+def test_select_level_takes_float_usage(cuda_device):
+    """The reference's signature takes floats (controller.py:81): fractional
+    usage and capacity are not truncated."""
+    rng = np.random.default_rng(4)
+    n = 20_000
+    usage = rng.uniform(0, 2.0, n)
+    cap = rng.uniform(0.1, 1.5, n)
+    L = rng.integers(2, 17, n)
+    alpha = rng.choice([0.5, 0.75, 1.0], n)
+    got = ops.select_level_batch(usage, cap, L, alpha)
+    want = [asb.select_frequency_level(u, c, int(lv), a) for u, c, lv, a in zip(usage, cap, L, alpha)]
+    assert got.tolist() == want
+    assert ops.select_level_batch([0.5], [1.0], [4], [0.75])[0] == 3
+
+
 def oracle_assign(usages, capacity, theta):
     light = [i for i in range(1, len(usages) + 1) if usages[i - 1] < theta * capacity]
     if light:
@@ -96,20 +111,3 @@ def test_min_throughput_reduction(cuda_device):
             assert got[s] == min(vals)
         else:
             assert math.isnan(got[s])
-
-
-def test_scalar_api_mirror(cuda_device):
-    assert asb.select_frequency_level(37_500, 100_000, 7, 0.75) == 4
-    assert asb.select_frequency_level(75_000, 100_000, 7, 0.75) == 7
-    lvl = asb.FrequencyLevel(1000.0, 10000.0, 1000.0, 300.0, 50.0)
-    cfg = asb.InstanceConfig(thrash_latency_factor=3.0)
-    assert asb.service_time(asb.TurnRecord(1000, 100, 0.0), lvl, 0, 1, True, cfg) == pytest.approx(0.6, rel=1e-12)
-    state = asb.RouterState(instance_ids=[1, 2, 3, 4])
-    agent = asb.AgentRuntimeState("a")
-    assert asb.assign_agent(agent, {1: 60_000, 2: 10_000, 3: 0, 4: 0}, 100_000, asb.RouterConfig(), state) == 2
-    agent = asb.AgentRuntimeState("b", instance_id=1, steps_since_assignment=7)
-    assert asb.maybe_reassign(agent, {1: 80_000, 2: 30_000}, asb.RouterConfig(), asb.RouterState([1, 2])) == 2
-    a = asb.AgentRuntimeState("c", decode_tokens_total=300, llm_time_total=15.0)
-    assert asb.running_throughput(a) == 20.0
-    assert asb.running_throughput(asb.AgentRuntimeState("d")) is None
-    assert asb.slo_boost_check([a, asb.AgentRuntimeState("e", decode_tokens_total=50, llm_time_total=10.0)], 20.0)

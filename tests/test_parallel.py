@@ -17,7 +17,8 @@ import torch.multiprocessing as mp
 import paper_2604_16682_b200 as asb
 from paper_2604_16682_b200 import _abi
 from paper_2604_16682_b200.engine import prepare_batch
-from paper_2604_16682_b200.parallel import allreduce_stats, gather_rows, partition_lpt, scenario_weights
+from paper_2604_16682_b200.parallel import (allreduce_stats, check_status_all, config_weights, gather_rows,
+                                            partition_lpt, scenario_weights)
 
 
 def test_partition_lpt_covers_and_balances():
@@ -43,6 +44,16 @@ def test_partition_lpt_more_ranks_than_scenarios():
     assert sorted(len(p) for p in parts) == [0, 0, 1, 1]
     with pytest.raises(ValueError):
         partition_lpt([1], 0)
+
+
+def test_config_weights_without_packing():
+    tr = asb.generate_workload(asb.WorkloadSpec(arrival_rate=0.4, duration=50.0, seed=1))
+    spec = asb.WorkloadSpec(arrival_rate=2.0, duration=100.0, seed=3)
+    cfgs = [asb.SimConfig(traces=tr), asb.SimConfig(workload=spec), asb.SimConfig(workload=spec, seed=9)]
+    w = config_weights(cfgs)
+    assert w[0] == sum(len(t.turns) for t in tr)
+    assert w[1] == w[2] == int(2.0 * 100.0 * spec.turn_count.mean)
+    assert np.array_equal(w, config_weights(cfgs))
 
 
 def _configs():
@@ -94,6 +105,16 @@ def _worker(rank, world, port, q):
         ok_rows = np.array_equal(got_stats.view(np.uint8), stats.view(np.uint8)) and np.array_equal(got_ctr, ctr)
         want = host_fold(stats, ctr)
         ok_red = np.allclose(red.numpy(), want, rtol=1e-12, atol=0) and np.array_equal(red.numpy()[2:], want[2:])
+        # a device status on ONE rank raises on EVERY rank (no partial aggregates)
+        check_status_all(c_loc)
+        bad = c_loc.clone()
+        if rank == 1 and bad.numel():
+            bad[_abi.CTR["status"]] = 3
+        try:
+            check_status_all(bad)
+            ok_red = False
+        except asb.SimulationError:
+            pass
         q.put((rank, bool(ok_rows), bool(ok_red), len(owned)))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent

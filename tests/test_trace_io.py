@@ -26,8 +26,11 @@ def assert_same(a, b):
 
 def native_rc(path):
     lib = _trace_io()
+    h = C.c_void_p()
     na, nt, nb, bad = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
-    return lib.asb_trace_scan(str(path).encode(), C.byref(na), C.byref(nt), C.byref(nb), C.byref(bad)), bad.value
+    rc = lib.asb_trace_parse(str(path).encode(), C.byref(h), C.byref(na), C.byref(nt), C.byref(nb), C.byref(bad))
+    lib.asb_trace_free(h)
+    return rc, bad.value
 
 
 @pytest.mark.parametrize("seed", [0, 7])
@@ -47,7 +50,8 @@ def test_accepted_variations(tmp_path):
         '"agent_id": "a\\"1"}  \n'
         '\n'
         '{"agent_id":"a2","arrival_time":0.1,"turns":[[1,1,-0.0]],"turns":[[5,6,7.25]],"extra":true}\n'
-        '{"agent_id": "é", "arrival_time": -0, "turns": [[2147483647, 1, 1e-300]]}\n',
+        '{"agent_id": "é", "arrival_time": -0, "turns": [[2147483647, 1, 1e-300]]}\n'
+        '{"agent_id": "b", "arrival_time": 0.5E+1, "turns": [[10E0, 2, 0e-5], [3, 1, 1.25e1]]}\n',
         encoding="utf-8")
     assert native_rc(p) == (0, 0)
     assert_same(load_trace_arrays(str(p)), python_arrays(str(p)))
@@ -64,6 +68,15 @@ BAD = [
     ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1]]}', TraceFormatError),
     ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1, 1.0]]', TraceFormatError),
     ('[1, 2]', TraceFormatError),
+    # numbers outside the JSON grammar: json.loads rejects them, so must the fast path
+    ('{"agent_id": "a", "arrival_time": 1., "turns": [[1, 1, 1.0]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": .5, "turns": [[1, 1, 1.0]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[0400, 1, 1.0]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1, 1e]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1, -]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": +1.0, "turns": [[1, 1, 1.0]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1, 1.0e+]]}', TraceFormatError),
+    ('{"agent_id": "a", "arrival_time": 00, "turns": [[1, 1, 1.0]]}', TraceFormatError),
     ('{"agent_id": "a", "arrival_time": 1.0, "turns": [[1, 1, 1.0]]}\n'
      '{"agent_id": "a", "arrival_time": 2.0, "turns": [[1, 1, 1.0]]}', TraceFormatError),
 ]
