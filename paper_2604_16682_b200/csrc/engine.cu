@@ -92,6 +92,8 @@ EC_DEV double ec_floor(double x) { return floor(x); }
 EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__double_as_longlong(x); }
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 EC_DEV long long ec_clock() { return clock64(); }
+EC_DEV float ec_f32_down(double x) { return __double2float_rd(x); } /* rounded toward -inf: <= x */
+#define EC_INF_F32 __int_as_float(0x7f800000)
 #define EC_TID ((int)threadIdx.x)
 /* named CTA barriers for the fork-join team.  Each warp reconverges first
  * (__syncwarp): a warp that reaches a CTA barrier with some lanes still
@@ -156,11 +158,6 @@ EC_DEV unsigned long long l2_keep() {
   asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-EC_DEV double ldk_f64(const double* p) {
-  double v;
-  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_keep()));
-  return v;
-}
 EC_DEV int ldk_i32(const int* p) {
   int v;
   asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_keep()));
@@ -172,21 +169,28 @@ EC_DEV void stk_f64(double* p, double v) {
 EC_DEV void stk_i32(int* p, int v) {
   asm volatile("st.global.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(l2_keep()) : "memory");
 }
-/* two consecutive slots in one 16-byte (f64) / 8-byte (i32) load */
-EC_DEV void ldk_f64x2(const double* p, double& a, double& b) {
-  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-               : "=d"(a), "=d"(b) : "l"(p), "l"(l2_keep()));
+/* a whole 16-byte alive slot in one vector load */
+template <class S>
+EC_DEV void ldk_slot(const S* p, double& tp, float& nx, int& meta) {
+  unsigned long long lo, hi;
+  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.v2.b64 {%0, %1}, [%2], %3;"
+               : "=l"(lo), "=l"(hi) : "l"(p), "l"(l2_keep()));
+  tp = __longlong_as_double((long long)lo);
+  nx = __int_as_float((int)(unsigned)hi);
+  meta = (int)(unsigned)(hi >> 32);
 }
-EC_DEV void ldk_i32x2(const int* p, int& a, int& b) {
-  asm volatile("ld.global" ASB_L1_KEEP ".L2::cache_hint.v2.s32 {%0, %1}, [%2], %3;"
-               : "=r"(a), "=r"(b) : "l"(p), "l"(l2_keep()));
+/* the slot's (nx, meta) half in one 8-byte store */
+template <class S>
+EC_DEV void stk_ev(S* p, float nx, int meta) {
+  const unsigned long long v = (unsigned long long)(unsigned)__float_as_int(nx) | ((unsigned long long)(unsigned)meta << 32);
+  asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(&p->nx), "l"(v), "l"(l2_keep()) : "memory");
 }
-#define EC_LDK_F64(p) ldk_f64(p)
 #define EC_LDK_I32(p) ldk_i32(p)
-#define EC_LDK_F64X2(p, a, b) ldk_f64x2((p), (a), (b))
-#define EC_LDK_I32X2(p, a, b) ldk_i32x2((p), (a), (b))
 #define EC_STK_F64(p, v) stk_f64((p), (v))
 #define EC_STK_I32(p, v) stk_i32((p), (v))
+#define EC_LDK_SLOT(p, tp_, nx_, mt_) ldk_slot((p), (tp_), (nx_), (mt_))
+#define EC_STK_EV(p, nx_, mt_) stk_ev((p), (nx_), (mt_))
+#define EC_SLOT_ACCESSORS /* the cache-hinted accessors above replace engine_core.h's defaults */
 #endif
 
 #include "engine_core.h"
@@ -195,8 +199,9 @@ namespace {
 
 struct Workspace {
   asb::AgentHot* hot;
-  double *notbefore, *pissue, *s_tp, *s_next, *arr_t;
-  int *alive, *s_meta, *dstamp;
+  asb::Slot* sl;
+  double *notbefore, *pissue, *arr_t;
+  int *alive, *dstamp;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -217,12 +222,10 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   Workspace t;
   t.hot = (asb::AgentHot*)take(na * sizeof(asb::AgentHot));
   t.arr_t = (double*)take(na * 8);
-  t.s_tp = (double*)take(na * 8);
-  t.s_next = (double*)take(na * 8);
+  t.sl = (asb::Slot*)take(na * sizeof(asb::Slot));
   t.notbefore = (double*)take(na * 8);
   t.pissue = (double*)take(na * 8);
   t.alive = (int*)take(na * 4);
-  t.s_meta = (int*)take(na * 4);
   t.dstamp = (int*)take(na * 4);
   t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
@@ -326,9 +329,7 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 4 : 1)
     g.o_mig = out.migrations + oa;
     g.o_phase = out.phase + oa;
     g.alive = ws.alive + oa;
-    g.s_tp = ws.s_tp + oa;
-    g.s_next = ws.s_next + oa;
-    g.s_meta = ws.s_meta + oa;
+    g.sl = ws.sl + oa;
     g.dstamp = ws.dstamp + oa;
     g.ring = ws.ring + ws.ring_off[s];
     g.log = ws.log + ws.ring_off[s];

@@ -42,6 +42,13 @@ static inline double ec_floor(double x) { return floor(x); }
 static inline unsigned long long ec_bits(double x) { unsigned long long b; memcpy(&b, &x, 8); return b; }
 static inline double ec_from_bits(unsigned long long b) { double x; memcpy(&x, &b, 8); return x; }
 static inline long long ec_clock() { return 0; }
+/* round toward -inf to f32 (<= x), as __double2float_rd */
+static inline float ec_f32_down(double x) {
+  float f = (float)x;
+  if ((double)f > x) f = nextafterf(f, -__builtin_inff());
+  return f;
+}
+#define EC_INF_F32 (__builtin_inff())
 #define EC_TID 0
 static inline void ec_fork_begin(int) {}
 static inline void ec_fork_end(int) {}
@@ -77,6 +84,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     double* f64 = (double*)calloc(na * 10, 8);
     asb::AgentHot* hot = (asb::AgentHot*)aligned_alloc(128, na * sizeof(asb::AgentHot));
     long long* i64 = (long long*)calloc(na * 2, 8);
+    asb::Slot* sl = (asb::Slot*)aligned_alloc(16, na * sizeof(asb::Slot));
     int* i32 = (int*)calloc(na * 7, 4);
     int* rl = (int*)calloc(na * (size_t)sc.n_instances * 2, 4);
     g.arrival = tp->arrival + a0;
@@ -88,7 +96,6 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.turn_base = tp->trace_turn_off[sc.trace_id];
     g.H = hot;
     g.ctime = out->completion_time + oa;
-    g.s_tp = f64 + 8 * na;
     g.arr_t = f64 + 9 * na;
     g.notbefore = f64 + 6 * na;
     g.pissue = f64 + 7 * na;
@@ -102,9 +109,8 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.o_mig = out->migrations + oa;
     g.o_phase = out->phase + oa;
     g.alive = i32 + 3 * na;
-    g.s_meta = i32 + 5 * na;
     g.dstamp = i32 + 6 * na;
-    g.s_next = f64;
+    g.sl = sl;
     g.ring = rl;
     g.log = rl + na * (size_t)sc.n_instances;
     g.turn_issue = out->turn_issue ? out->turn_issue + out->turn_off[s] : nullptr;
@@ -132,6 +138,7 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     free(f64);
     free(hot);
     free(i64);
+    free(sl);
     free(i32);
     free(rl);
   }

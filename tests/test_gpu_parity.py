@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 
 FULL = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "*.json.gz"))
               if not os.path.basename(p).startswith(("c3", "c4", "c5")))
-DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz")))
+DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz"))
+                if not os.path.basename(p).startswith("c4_full"))  # full C4: test_gpu_fullsize.py
 
 
 def gpu(batch, decisions=True, turn_log=True):

@@ -16,7 +16,10 @@ from oracle.oracle import run_oracle
 
 FULL = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "*.json.gz"))
               if not os.path.basename(p).startswith(("c3", "c4", "c5")))
-DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz")))
+# full C4 in both thrash modes is numerically one run (instance.py:121): the
+# oracle is pinned on "recompute"; the GPU suite checks both and the echo
+DIGEST = sorted(os.path.basename(p) for p in glob.glob(os.path.join(GOLDEN, "c[345]*.json.gz"))
+                if os.path.basename(p) != "c4_full_offload.json.gz")
 
 
 def golden_config(g):
