@@ -114,23 +114,53 @@ CONFIGS = {
 }
 
 
+def workload_spec(config: str, seed: int):
+    """The WorkloadSpec of one seed of a BASELINE config."""
+    import paper_2604_16682_b200 as asb
+
+    if config == "c5":
+        return asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=seed)
+    if config == "c3":
+        return asb.WorkloadSpec(arrival_rate=0.08, duration=12500.0, seed=seed)
+    if config == "c4":
+        return asb.WorkloadSpec(arrival_rate=100000 / 3600, duration=3600.0, seed=11 + seed,
+                                prefill_growth_per_turn=20)
+    raise ValueError(f"unknown config {config!r}")
+
+
+def _gen_one(job):
+    from paper_2604_16682_b200.workload import generate_workload_arrays
+
+    return generate_workload_arrays(workload_spec(*job))
+
+
+def generate_traces(config: str, seeds: list[int]) -> list[dict]:
+    """The reference's generate_workload stream for every seed (same numpy
+    draws, CSR arrays instead of objects), seeds in parallel on the host."""
+    jobs = [(config, s) for s in seeds]
+    workers = min(len(jobs), cpu_cores(), 32)
+    if workers <= 1:
+        return [_gen_one(j) for j in jobs]
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        return list(ex.map(_gen_one, jobs))
+
+
 def build_shard(rank: int, seeds_per_gpu: int | None = None, config: str = "c5"):
     import paper_2604_16682_b200 as asb
     from paper_2604_16682_b200 import _abi, packing
-    from paper_2604_16682_b200.workload import generate_arrays
 
     k = seeds_per_gpu or CONFIGS[config]["seeds_per_gpu"]
     seeds = list(range(rank * k, (rank + 1) * k))
+    arrs = generate_traces(config, seeds)
     if config == "c5":
-        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=10000 / 3600, duration=3600.0, seed=s)) for s in seeds]
         cells, tables = c5_cells(), [asb.default_frequency_table()]
     elif config == "c3":
-        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=0.08, duration=12500.0, seed=s)) for s in seeds]
         cells, table = c3_cells()
         tables = [table]
     elif config == "c4":
-        arrs = [generate_arrays(asb.WorkloadSpec(arrival_rate=100000 / 3600, duration=3600.0, seed=11 + s,
-                                                 prefill_growth_per_turn=20)) for s in seeds]
         cells = [asb.SimConfig(traces=[], instance_count=64, sim_duration=3600.0,
                                controller=asb.ControllerConfig(thrash_avoidance=False))]
         tables = [asb.default_frequency_table()]
@@ -139,6 +169,8 @@ def build_shard(rank: int, seeds_per_gpu: int | None = None, config: str = "c5")
     recs = [packing.scenario_record(c, t, 0) for t in range(len(seeds)) for c in cells]
     scen = np.array(recs, dtype=_abi.SCENARIO_DTYPE)
     batch = packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables(tables))
+    batch.cells = cells  # the SimConfig of scenario s is cells[s % len(cells)] on trace s // len(cells)
+    batch.trace_arrays = arrs
     return batch, seeds
 
 
@@ -251,6 +283,69 @@ def cpu_cores() -> int:
         return os.cpu_count() or 1
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # pip install --target of /root/reference/pkg (travels)
+PYREF_SCEN_PER_WORKER = {"c5": 1, "c3": 3}  # ~5-10 s of reference time per worker; C4 (70 s) is not sampled
+
+
+def _pyref_one(job):
+    """One scenario through the REFERENCE's own run_simulation (baseline/_ref),
+    on the same trace arrays and cell config the GPU ran."""
+    cell, arrs, ref_dir = job
+    if ref_dir not in sys.path:
+        sys.path.insert(0, ref_dir)
+    import agentsim as ref
+
+    from paper_2604_16682_b200.adapter import convert
+    from paper_2604_16682_b200.engine import agent_ticks_closed_form
+
+    arrival, off = arrs["arrival"], arrs["turn_off"]
+    pre, dec, tool = arrs["prefill"].tolist(), arrs["decode"].tolist(), arrs["tool"].tolist()
+    traces = [ref.AgentTrace(f"a{i:06d}", float(arrival[i]),
+                             tuple(ref.TurnRecord(pre[j], dec[j], tool[j]) for j in range(off[i], off[i + 1])))
+              for i in range(arrival.size)]
+    cfg = convert(cell, ref)
+    cfg.traces = traces
+    t0 = time.perf_counter()
+    res = ref.run_simulation(cfg)
+    sec = time.perf_counter() - t0
+    e = cfg.controller.epoch_length
+    k = 0
+    while k * e < cfg.sim_duration:
+        k += 1
+    arr = np.array([a.arrival_time for a in res.agents], dtype=np.float64)
+    comp = np.array([np.nan if a.completion_time is None else a.completion_time for a in res.agents])
+    return sec, agent_ticks_closed_form(arr, comp, e, k)
+
+
+def python_reference(batch, config: str):
+    """The reference's own Python path (agentsim.run_simulation from
+    baseline/_ref) on a bounded sample of the shard, one process per host
+    core, as the reference's sweep runs cells (cli.py:161-188)."""
+    per = PYREF_SCEN_PER_WORKER.get(config)
+    if per is None or not os.path.isdir(os.path.join(REF_DIR, "agentsim")):
+        why = "reference not installed in baseline/_ref" if per is not None else \
+            f"{config}: one reference scenario takes minutes; not sampled"
+        return {"unavailable": why}
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    workers = max(1, min(cpu_cores(), 64, batch.n // per))
+    n = workers * per
+    ncell = len(batch.cells)
+    jobs = [(batch.cells[s % ncell], batch.trace_arrays[s // ncell], REF_DIR) for s in range(n)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        out = list(ex.map(_pyref_one, jobs))
+    wall = time.perf_counter() - t0
+    sec = sum(o[0] for o in out)
+    ticks = sum(o[1] for o in out)
+    return {"value": ticks / sec * workers, "unit": UNIT, "cores": workers, "kind": "python-reference",
+            "per_core": ticks / sec,
+            "sample": f"the first {n} scenarios of the shard ({per} per process, {workers} processes, "
+                      f"{wall:.1f} s wall): agentsim.run_simulation from baseline/_ref (the unmodified reference), "
+                      "value = per-core rate x processes; trace object construction excluded"}
+
+
 def reference_arm(args, world, rank):
     """`--impl reference`: the CPU restatement of the reference on all host cores."""
     if rank != 0:
@@ -274,15 +369,17 @@ def reference_arm(args, world, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(batch, seeds, world, "cpu", args.config),
+        "config": config_block(batch, seeds, world, args.config),
+        "arm": f"CPU: serial C restatement of the reference (oracle/des_oracle.c), OpenMP over scenarios, {cores} threads",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"one {args.config.upper()} shard per step: {batch.n} scenarios (seeds {seeds[0]}-{seeds[-1]})"},
+        "python_reference": python_reference(batch, args.config),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def config_block(batch, seeds, world, parallel, config="c5"):
+def config_block(batch, seeds, world, config="c5"):
     cfg = CONFIGS[config]
     n_agents = batch.total_agents / max(batch.n, 1)
     tbytes = sum(getattr(batch.traces, k).nbytes for k in ("arrival", "agent_turn_off", "prefill", "decode", "tool"))
@@ -291,7 +388,7 @@ def config_block(batch, seeds, world, parallel, config="c5"):
         "scenarios_per_gpu": batch.n, "seeds_per_gpu": len(seeds), "instances": cfg["instances"],
         "mean_agents_per_scenario": round(n_agents, 1), "sim_duration_s": cfg["sim_duration_s"],
         "epochs": cfg["epochs"],
-        "parallelism": f"scenario-sharded x{world} ({parallel})",
+        "parallelism": f"scenario-sharded x{world}",
         "l2": f"inputs larger than L2: {tbytes / 2**20:.0f} MiB trace pool + workspace per GPU, no flush",
     }
 
@@ -445,7 +542,8 @@ def main():
 
     cpu = None
     parity = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    pyref = None
+    if rank == 0 and not args.no_cpu_baseline:
         _build.build_oracle()
         cores = cpu_cores()
         host_ref, stats_ref, sec = cpu_run(batch, cores)
@@ -460,19 +558,24 @@ def main():
         a = got["counters"].reshape(-1, _abi.ASB_NCOUNTERS)[:, :9]
         same = same and np.array_equal(a, ctr_ref[:, :9])
         parity = f"{'bit-exact' if same else 'MISMATCH'} vs oracle on all {batch.n} scenarios of the timed shard"
+        if world > 1:
+            parity += " (rank 0's shard)"
+            cpu["sample"] = "rank 0's shard: " + cpu["sample"]
+        pyref = python_reference(batch, args.config)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (vectorised generator, reference distributions)",
-            "config": config_block(batch, seeds, world, "nccl allreduce of stats" if world > 1 else "1 GPU",
-                                   args.config),
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic: the reference's generate_workload stream (same numpy default_rng draws, CSR arrays)",
+            "config": config_block(batch, seeds, world, args.config),
+            "arm": f"B200 x{world}" + (": NCCL allreduce of the stats vector" if world > 1 else ""),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "asb_engine_kernel", "kernel_ms": kern_s * 1e3,
                          "alg_bytes_per_launch": b_alg, "peak_source": peak_src},
             "cpu_baseline": cpu,
+            "python_reference": pyref,
             "e2e": e2e,
             "clocks": clk.summary(),
             "gpu_launches": 4 * args.steps,

@@ -201,7 +201,7 @@ struct Workspace {
   asb::AgentHot* hot;
   asb::Slot* sl;
   double *notbefore, *pissue, *arr_t;
-  int *alive, *dstamp;
+  int* dstamp;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -225,7 +225,6 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   t.sl = (asb::Slot*)take(na * sizeof(asb::Slot));
   t.notbefore = (double*)take(na * 8);
   t.pissue = (double*)take(na * 8);
-  t.alive = (int*)take(na * 4);
   t.dstamp = (int*)take(na * 4);
   t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
@@ -328,7 +327,6 @@ __global__ void __launch_bounds__(NT, NT <= 128 ? 4 : 1)
     g.o_inst = out.final_instance + oa;
     g.o_mig = out.migrations + oa;
     g.o_phase = out.phase + oa;
-    g.alive = ws.alive + oa;
     g.sl = ws.sl + oa;
     g.dstamp = ws.dstamp + oa;
     g.ring = ws.ring + ws.ring_off[s];
@@ -415,6 +413,14 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   Workspace ws;
   carve((unsigned char*)d_workspace, n_scen, total_agents, total_ring_slots, &ws);
   cudaStream_t st = (cudaStream_t)stream;
+  if (const char* pl = getenv("ASB_L2_PERSIST_MB")) { /* experiment: L2 set-aside for evict_last lines */
+    size_t want = (size_t)atol(pl) << 20;
+    int dev0 = 0, mx = 0;
+    cudaGetDevice(&dev0);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev0);
+    if (want > (size_t)mx) want = (size_t)mx;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  }
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
   /* team shape by scenario size (ASB_TEAM=solo|quad|big overrides, for tests):

@@ -28,7 +28,8 @@ from .errors import ConfigurationError, SimulationError
 from .instance import InstanceConfig
 from .metrics import AgentMetrics, SystemMetrics
 from .router import RouterConfig
-from .workload import AgentTrace, WorkloadSpec, generate_workload, load_trace, load_trace_arrays
+from .workload import (AgentTrace, WorkloadSpec, generate_workload, generate_workload_arrays, load_trace,
+                       load_trace_arrays)
 
 
 @dataclass
@@ -247,11 +248,35 @@ def _resolve(config: SimConfig, key) -> list[AgentTrace]:
     return traces
 
 
-def prepare_batch(configs: Sequence[SimConfig]) -> packing.Batch:
+def _generate_specs(specs: list, workers: int | None) -> dict:
+    """generate_workload_arrays of many WorkloadSpecs, in worker processes
+    when there are many (each seed is an independent numpy stream)."""
+    import os
+
+    if workers is None:
+        try:
+            workers = len(os.sched_getaffinity(0))
+        except AttributeError:
+            workers = os.cpu_count() or 1
+    workers = min(workers, len(specs), 32)
+    if workers <= 1 or len(specs) < 16:
+        return {sp: generate_workload_arrays(sp) for sp in specs}
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        return dict(zip(specs, ex.map(generate_workload_arrays, specs)))
+
+
+def prepare_batch(configs: Sequence[SimConfig], workers: int | None = None) -> packing.Batch:
     """Validate (raising ConfigurationError before any device work), resolve
-    and de-duplicate traces and tables, and pack the batch."""
+    and de-duplicate traces and tables, and pack the batch.  Distinct
+    WorkloadSpecs are generated in ``workers`` processes (default: the host's
+    cores) when there are 16 or more."""
     for c in configs:
         c.validate()
+    specs = list(dict.fromkeys(k[1] for k in map(_trace_key, configs) if k[0] == "spec"))
+    generated = _generate_specs(specs, workers) if specs else {}
     trace_index: dict = {}
     trace_arrays: list[dict] = []
     table_index: dict = {}
@@ -266,6 +291,11 @@ def prepare_batch(configs: Sequence[SimConfig]) -> packing.Batch:
                 ids = arrs["agent_ids"]
                 if len(set(ids)) != len(ids):  # the reference's duplicate check and message
                     _resolve(c, key)
+            elif key[0] == "spec":
+                # generate_workload's exact draws straight into CSR arrays; its
+                # ids are "a%06d" by position (unique), built only on demand
+                arrs = generated[key[1]]
+                arrs["agent_ids"] = None
             else:
                 arrs = packing.trace_arrays_from_objects(_resolve(c, key))
             trace_arrays.append(arrs)
@@ -405,13 +435,17 @@ def check_status(host: Mapping, n: int) -> None:
 
 
 def build_results(batch: packing.Batch, host: Mapping, stats: np.ndarray, configs: Sequence[SimConfig],
-                  echos: Sequence[dict | None]) -> list[SimulationResult]:
-    """Rebuild the reference's SimulationResult objects from output arrays."""
-    check_status(host, batch.n)
+                  echos: Sequence[dict | None], only: Sequence[int] | None = None,
+                  checked: bool = False) -> list[SimulationResult]:
+    """Rebuild the reference's SimulationResult objects from output arrays
+    (every scenario, or the scenarios listed in ``only``)."""
+    if not checked:
+        check_status(host, batch.n)
     tp = batch.traces
     results = []
     ctr_all = host["counters"].reshape(batch.n, _abi.ASB_NCOUNTERS)
-    for s, cfg in enumerate(configs):
+    for s in (range(len(configs)) if only is None else only):
+        cfg = configs[s]
         rec = batch.scen[s]
         t = int(rec["trace_id"])
         a0, a1 = int(batch.agent_off[s]), int(batch.agent_off[s + 1])
@@ -512,16 +546,81 @@ def build_results(batch: packing.Batch, host: Mapping, stats: np.ndarray, config
     return results
 
 
+class BatchResult(Sequence):
+    """Columnar results of ``run_simulation_batch(..., columnar=True)``.
+
+    The engine's output arrays as downloaded, without a Python object per
+    agent: ``system`` (one SystemMetrics row per scenario: slo_attainment,
+    p5_throughput, job_throughput, average_power, energy, thrash_fraction;
+    NaN = None), ``counters`` (arrived, completed, agent-ticks, ... per
+    scenario), ``agents(s)`` / ``instances(s)`` (numpy columns of scenario s,
+    agents in arrival order like ``SimulationResult.agents``) and ``arrays``
+    (every output array; agent rows of scenario s at
+    ``batch.agent_off[s]:batch.agent_off[s+1]``).  Indexing builds scenario
+    s's full ``SimulationResult`` (the reference's types) on first access.
+    Device status words are checked at construction (SimulationError).
+    """
+
+    def __init__(self, batch: packing.Batch, host: Mapping, stats: np.ndarray, configs: Sequence[SimConfig],
+                 echos: Sequence[dict | None] | None):
+        check_status(host, batch.n)
+        self.batch, self.arrays, self.system = batch, host, stats
+        self.configs, self.echos = list(configs), echos
+        self.counters = host["counters"].reshape(batch.n, _abi.ASB_NCOUNTERS)
+        self._cache: dict[int, SimulationResult] = {}
+
+    def __len__(self) -> int:
+        return self.batch.n
+
+    def __getitem__(self, s):
+        if isinstance(s, slice):
+            return [self[i] for i in range(*s.indices(len(self)))]
+        s = range(len(self))[s]
+        if s not in self._cache:
+            (self._cache[s],) = build_results(self.batch, self.arrays, self.system, self.configs, self.echos,
+                                              only=[s], checked=True)
+        return self._cache[s]
+
+    def counter(self, name: str) -> np.ndarray:
+        return self.counters[:, _abi.CTR[name]]
+
+    def agents(self, s: int) -> dict[str, np.ndarray]:
+        """Per-agent columns of scenario s (arrived agents, arrival order)."""
+        a0, a1 = int(self.batch.agent_off[s]), int(self.batch.agent_off[s + 1])
+        rank = self.arrays["arrival_rank"][a0:a1]
+        arrived = np.nonzero(rank >= 0)[0]
+        order = arrived[np.argsort(rank[arrived], kind="stable")]
+        t = int(self.batch.scen[s]["trace_id"])
+        g0 = int(self.batch.traces.trace_agent_off[t])
+        cols = {k: self.arrays[k][a0:a1][order] for k in _abi.AGENT_OUT}
+        cols["arrival_time"] = self.batch.traces.arrival[g0 + order]
+        llm, dec = cols["llm_time"], cols["decode_total"]
+        with np.errstate(divide="ignore", invalid="ignore"):
+            cols["throughput"] = np.where(llm > 0, dec / np.where(llm > 0, llm, 1.0), np.nan)
+        cols["index"] = order
+        return cols
+
+    def instances(self, s: int) -> dict[str, np.ndarray]:
+        i0, i1 = int(self.batch.inst_off[s]), int(self.batch.inst_off[s + 1])
+        return {k: self.arrays[k][i0:i1] for k in _abi.INST_OUT}
+
+
 def run_simulation_batch(configs: Sequence[SimConfig], config_echos: Sequence[dict | None] | None = None, *,
                          device=None, decisions: bool = True, turn_log: bool = True,
-                         timeseries: bool = False) -> list[SimulationResult]:
+                         timeseries: bool = False, columnar: bool = False):
     """Run many independent simulations on one GPU; each result equals the
     reference's ``run_simulation`` of the same config (``timeseries`` rows
-    only when asked for: those scenarios take the exact serial loop)."""
+    only when asked for: those scenarios take the exact serial loop).
+
+    ``columnar=True`` returns a ``BatchResult`` (numpy columns, per-scenario
+    ``SimulationResult`` built lazily) instead of a list of results: at
+    sweep scale the per-agent objects would cost far more than the run."""
     batch = prepare_batch(configs)
     dev_batch = DeviceBatch(batch, device=device, decisions=decisions, turn_log=turn_log, timeseries=timeseries)
     dev_batch.run()
     host, stats = dev_batch.download()
+    if columnar:
+        return BatchResult(batch, host, stats, configs, config_echos)
     return build_results(batch, host, stats, configs, config_echos)
 
 

@@ -161,6 +161,9 @@ def epoch_count(sim_duration: float, epoch_length: float) -> int:
     return k
 
 
+MAX_AGENTS = 1 << 21  # agent ids live in 21 bits of the engine's alive-slot word (engine_core.h Slot)
+
+
 def scenario_record(config, trace_id: int, table_id: int) -> tuple:
     """One AsbScenario row for a validated SimConfig."""
     inst = config.instance
@@ -252,6 +255,8 @@ def build_batch(scen: np.ndarray, traces: TracePool, tables: TablePool) -> Batch
     n = scen.size
     tid = scen["trace_id"].astype(np.int64)
     a_cnt = traces.trace_agent_off[tid + 1] - traces.trace_agent_off[tid]
+    if n and int(a_cnt.max()) >= MAX_AGENTS:
+        raise ConfigurationError(f"workload: the B200 engine supports at most {MAX_AGENTS - 1} agents per scenario")
     t_cnt = traces.trace_turn_off[tid + 1] - traces.trace_turn_off[tid]
     m = scen["n_instances"].astype(np.int64)
 

@@ -25,12 +25,20 @@ from paper_2604_16682_b200 import _abi  # noqa: E402
 from paper_2604_16682_b200.engine import build_results, prepare_batch  # noqa: E402
 
 
-def reference_module():
-    """The reference package (read-only tree), or None when absent (GPU box)."""
-    if not os.path.isdir(REF_SRC):
+REF_INSTALLED = os.path.join(ROOT, "baseline", "_ref")  # pip install --target of the reference (travels)
+
+
+def reference_module(installed: bool = False):
+    """The reference package: the read-only tree in the build container, or
+    (``installed=True``) its pip install under baseline/_ref, which also
+    exists on the GPU box when it was installed; None when absent."""
+    path = REF_SRC if os.path.isdir(REF_SRC) else None
+    if path is None and installed and os.path.isdir(os.path.join(REF_INSTALLED, "agentsim")):
+        path = REF_INSTALLED
+    if path is None:
         return None
-    if REF_SRC not in sys.path:
-        sys.path.insert(0, REF_SRC)
+    if path not in sys.path:
+        sys.path.insert(0, path)
     import agentsim  # noqa: F401
 
     return sys.modules["agentsim"]

@@ -108,7 +108,6 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
     g.o_inst = out->final_instance + oa;
     g.o_mig = out->migrations + oa;
     g.o_phase = out->phase + oa;
-    g.alive = i32 + 3 * na;
     g.dstamp = i32 + 6 * na;
     g.sl = sl;
     g.ring = rl;

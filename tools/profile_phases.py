@@ -24,9 +24,9 @@ from paper_2604_16682_b200.engine import DeviceBatch  # noqa: E402
 PHASES = ("tick_sweep+due", "epoch_instances", "arrivals+speculate", "sort", "walk", "apply+serial")
 if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
-if SWEEP:  # slots 2, 3 are event counts per epoch, not cycles
-    PHASES = ("tick_fork_cycles", "collect_due_cycles", "epoch_job_forks", "bisections", "due_total_cycles",
-              "admit_job_forks")
+if SWEEP:  # slots 3, 5 are event counts per epoch, not cycles
+    PHASES = ("tick_fork_cycles", "collect_due_cycles", "helper_in_tick_sweep_cycles", "bisections",
+              "due_total_cycles", "admit_job_forks")
     WALK = True
 
 
