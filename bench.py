@@ -70,32 +70,31 @@ C3_MHZ = (660.0, 810.0, 900.0, 1035.0, 1185.0, 1350.0, 1515.0, 1680.0)
 C3_CAPS = (250_000, 500_000, 750_000, 1_000_000)
 
 
-def c5_cells():
-    """C5 cells: router {context_aware, round_robin} x controller {context_aware, off} x tau {20, 35}."""
+def base_config(config: str):
+    """The experiment every cell of a BASELINE sweep applies to."""
     import paper_2604_16682_b200 as asb
 
-    cells = []
-    for pol in ("context_aware", "round_robin"):
-        for var in ("context_aware", "off"):
-            for tau in (20.0, 35.0):
-                cells.append(asb.SimConfig(traces=[], instance_count=16, sim_duration=3600.0,
-                                           controller=asb.ControllerConfig(variant=var, slo_target=tau),
-                                           router=asb.RouterConfig(policy=pol)))
-    return cells
+    if config == "c5":
+        return asb.SimConfig(workload=workload_spec("c5", 0), instance_count=16, sim_duration=3600.0)
+    if config == "c3":
+        return asb.SimConfig(workload=workload_spec("c3", 0), instance_count=1, sim_duration=12500.0,
+                             instance=asb.InstanceConfig(frequency_table=asb.default_frequency_table(mhz=C3_MHZ)))
+    if config == "c4":
+        return asb.SimConfig(workload=workload_spec("c4", 0), instance_count=64, sim_duration=3600.0,
+                             controller=asb.ControllerConfig(thrash_avoidance=False))
+    raise ValueError(f"unknown config {config!r}")
 
 
-def c3_cells():
-    """C3 DVFS sweep cells: 8 fixed frequency levels x 4 capacities (BASELINE configs[2])."""
-    import paper_2604_16682_b200 as asb
-
-    table = asb.default_frequency_table(mhz=C3_MHZ)
-    cells = []
-    for mhz in C3_MHZ:
-        for cap in C3_CAPS:
-            cells.append(asb.SimConfig(traces=[], instance_count=1, sim_duration=12500.0,
-                                       instance=asb.InstanceConfig(capacity_tokens=cap, frequency_table=table),
-                                       controller=asb.ControllerConfig(variant="fixed", fixed_level_mhz=mhz)))
-    return cells, table
+def sweep_axes(config: str, seeds: list[int]) -> dict:
+    """The BASELINE sweep as axes of the sweep driver (sweep.ALL_AXES)."""
+    if config == "c5":  # 8 cells: router x controller x SLO target, per seed
+        return {"slo_target": [20.0, 35.0], "policy": ["context_aware", "round_robin"],
+                "variant": ["context_aware", "off"], "seed": seeds}
+    if config == "c3":  # 8 fixed levels x 4 capacities, per seed
+        return {"level_mhz": list(C3_MHZ), "capacity": list(C3_CAPS), "seed": seeds}
+    if config == "c4":
+        return {"seed": [11 + s for s in seeds]}
+    raise ValueError(f"unknown config {config!r}")
 
 
 # workload table: seeds per GPU (weak scaling: rank r takes seeds [r*k, (r+1)*k)), generator, cells
@@ -111,7 +110,16 @@ CONFIGS = {
                                        "prefill growth 20/turn, 64 instances, context-aware without thrash avoidance, "
                                        "3600 s",
            "instances": 64, "epochs": 3600, "sim_duration_s": 3600.0},
+    # the whole C5 job (4096 scenarios) split over the N GPUs: strong scaling,
+    # N=1 runs all of it on one GPU
+    "c5full": {"seeds_total": 512, "desc": "C5 Monte-Carlo sweep, whole job: 4096 scenarios (512 seeds x 8 cells) "
+                                          "split over the GPUs, 16 instances x ~10k agents, 3600 s",
+               "instances": 16, "epochs": 3600, "sim_duration_s": 3600.0, "same_as": "c5"},
 }
+
+
+def scaling_of(config: str) -> str:
+    return "strong" if "seeds_total" in CONFIGS[config] else "weak"
 
 
 def workload_spec(config: str, seed: int):
@@ -123,54 +131,31 @@ def workload_spec(config: str, seed: int):
     if config == "c3":
         return asb.WorkloadSpec(arrival_rate=0.08, duration=12500.0, seed=seed)
     if config == "c4":
-        return asb.WorkloadSpec(arrival_rate=100000 / 3600, duration=3600.0, seed=11 + seed,
-                                prefill_growth_per_turn=20)
+        return asb.WorkloadSpec(arrival_rate=100000 / 3600, duration=3600.0, seed=seed, prefill_growth_per_turn=20)
     raise ValueError(f"unknown config {config!r}")
 
 
-def _gen_one(job):
-    from paper_2604_16682_b200.workload import generate_workload_arrays
-
-    return generate_workload_arrays(workload_spec(*job))
-
-
-def generate_traces(config: str, seeds: list[int]) -> list[dict]:
-    """The reference's generate_workload stream for every seed (same numpy
-    draws, CSR arrays instead of objects), seeds in parallel on the host."""
-    jobs = [(config, s) for s in seeds]
-    workers = min(len(jobs), cpu_cores(), 32)
-    if workers <= 1:
-        return [_gen_one(j) for j in jobs]
-    import multiprocessing as mp
-    from concurrent.futures import ProcessPoolExecutor
-
-    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
-        return list(ex.map(_gen_one, jobs))
-
-
 def build_shard(rank: int, seeds_per_gpu: int | None = None, config: str = "c5"):
-    import paper_2604_16682_b200 as asb
-    from paper_2604_16682_b200 import _abi, packing
+    """This rank's share of a BASELINE sweep, built through the public API:
+    sweep.sweep_cells over the sweep's axes (seed included), apply_cell to
+    the base experiment, prepare_batch (the reference's generate_workload
+    draws as CSR arrays, one trace per seed shared by its cells)."""
+    from paper_2604_16682_b200 import sweep
+    from paper_2604_16682_b200.engine import prepare_batch
 
-    k = seeds_per_gpu or CONFIGS[config]["seeds_per_gpu"]
-    seeds = list(range(rank * k, (rank + 1) * k))
-    arrs = generate_traces(config, seeds)
-    if config == "c5":
-        cells, tables = c5_cells(), [asb.default_frequency_table()]
-    elif config == "c3":
-        cells, table = c3_cells()
-        tables = [table]
-    elif config == "c4":
-        cells = [asb.SimConfig(traces=[], instance_count=64, sim_duration=3600.0,
-                               controller=asb.ControllerConfig(thrash_avoidance=False))]
-        tables = [asb.default_frequency_table()]
+    cfg = CONFIGS[config]
+    if "seeds_total" in cfg:  # strong scaling: the job's seeds split over the ranks
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        total = seeds_per_gpu or cfg["seeds_total"]
+        seeds = list(range(total * rank // world, total * (rank + 1) // world))
     else:
-        raise ValueError(f"unknown config {config!r}")
-    recs = [packing.scenario_record(c, t, 0) for t in range(len(seeds)) for c in cells]
-    scen = np.array(recs, dtype=_abi.SCENARIO_DTYPE)
-    batch = packing.build_batch(scen, packing.pack_traces(arrs), packing.pack_tables(tables))
-    batch.cells = cells  # the SimConfig of scenario s is cells[s % len(cells)] on trace s // len(cells)
-    batch.trace_arrays = arrs
+        k = seeds_per_gpu or cfg["seeds_per_gpu"]
+        seeds = list(range(rank * k, (rank + 1) * k))
+    config = cfg.get("same_as", config)
+    base = base_config(config)
+    configs = [sweep.apply_cell(base, c) for c in sweep.sweep_cells(sweep_axes(config, seeds))]
+    batch = prepare_batch(configs)
+    batch.configs = configs
     return batch, seeds
 
 
@@ -287,6 +272,16 @@ REF_DIR = os.path.join(ROOT, "baseline", "_ref")  # pip install --target of /roo
 PYREF_SCEN_PER_WORKER = {"c5": 1, "c3": 3}  # ~5-10 s of reference time per worker; C4 (70 s) is not sampled
 
 
+def trace_arrays_of(batch, s: int) -> dict:
+    """The CSR trace scenario s runs, sliced from the packed pool."""
+    tp = batch.traces
+    t = int(batch.scen[s]["trace_id"])
+    a0, a1 = int(tp.trace_agent_off[t]), int(tp.trace_agent_off[t + 1])
+    t0, t1 = int(tp.trace_turn_off[t]), int(tp.trace_turn_off[t + 1])
+    return {"arrival": tp.arrival[a0:a1], "turn_off": tp.agent_turn_off[a0:a1 + 1] - t0,
+            "prefill": tp.prefill[t0:t1], "decode": tp.decode[t0:t1], "tool": tp.tool[t0:t1]}
+
+
 def _pyref_one(job):
     """One scenario through the REFERENCE's own run_simulation (baseline/_ref),
     on the same trace arrays and cell config the GPU ran."""
@@ -304,7 +299,7 @@ def _pyref_one(job):
                              tuple(ref.TurnRecord(pre[j], dec[j], tool[j]) for j in range(off[i], off[i + 1])))
               for i in range(arrival.size)]
     cfg = convert(cell, ref)
-    cfg.traces = traces
+    cfg.workload, cfg.seed, cfg.traces = None, None, traces  # the same trace, generation not timed
     t0 = time.perf_counter()
     res = ref.run_simulation(cfg)
     sec = time.perf_counter() - t0
@@ -331,8 +326,8 @@ def python_reference(batch, config: str):
 
     workers = max(1, min(cpu_cores(), 64, batch.n // per))
     n = workers * per
-    ncell = len(batch.cells)
-    jobs = [(batch.cells[s % ncell], batch.trace_arrays[s // ncell], REF_DIR) for s in range(n)]
+    picks = [round(q * batch.n / n) for q in range(n)]  # spread over the shard's cells and seeds
+    jobs = [(batch.configs[s], trace_arrays_of(batch, s), REF_DIR) for s in picks]
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
         out = list(ex.map(_pyref_one, jobs))
@@ -341,7 +336,7 @@ def python_reference(batch, config: str):
     ticks = sum(o[1] for o in out)
     return {"value": ticks / sec * workers, "unit": UNIT, "cores": workers, "kind": "python-reference",
             "per_core": ticks / sec,
-            "sample": f"the first {n} scenarios of the shard ({per} per process, {workers} processes, "
+            "sample": f"{n} scenarios spread evenly over the shard ({per} per process, {workers} processes, "
                       f"{wall:.1f} s wall): agentsim.run_simulation from baseline/_ref (the unmodified reference), "
                       "value = per-core rate x processes; trace object construction excluded"}
 
@@ -367,13 +362,13 @@ def reference_arm(args, world, rank):
     value = ticks / sec
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": scaling_of(args.config),
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(batch, seeds, world, args.config),
         "arm": f"CPU: serial C restatement of the reference (oracle/des_oracle.c), OpenMP over scenarios, {cores} threads",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"one {args.config.upper()} shard per step: {batch.n} scenarios (seeds {seeds[0]}-{seeds[-1]})"},
-        "python_reference": python_reference(batch, args.config),
+        "python_reference": python_reference(batch, CONFIGS[args.config].get("same_as", args.config)),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -561,12 +556,12 @@ def main():
         if world > 1:
             parity += " (rank 0's shard)"
             cpu["sample"] = "rank 0's shard: " + cpu["sample"]
-        pyref = python_reference(batch, args.config)
+        pyref = python_reference(batch, CONFIGS[args.config].get("same_as", args.config))
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": scaling_of(args.config),
             "vs_baseline": None, "dtype": "f64", "data": "synthetic: the reference's generate_workload stream (same numpy default_rng draws, CSR arrays)",
             "config": config_block(batch, seeds, world, args.config),
             "arm": f"B200 x{world}" + (": NCCL allreduce of the stats vector" if world > 1 else ""),

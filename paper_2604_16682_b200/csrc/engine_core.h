@@ -77,6 +77,15 @@
 
 /* EC_DBG(slot, value): progress markers for hang debugging (GPU debug build
  * -DASB_DEBUG_TRACE writes them to host-mapped memory); no-op otherwise */
+/* EC_EPOCH_SYNC(nt): an includer hook run by the main warp at the start of
+ * every control epoch (the GPU lockstep kernels align the teams sharing a
+ * CTA there); no-op by default */
+#ifndef EC_EPOCH_SYNC
+#define EC_EPOCH_SYNC(nt) \
+  do {                    \
+  } while (0)
+#endif
+
 #ifndef EC_DBG
 #define EC_DBG(slot, value) \
   do {                      \
@@ -1034,7 +1043,7 @@ EC_DEV void fork_job(W* w, int job) {
   EC_LANE0 w->job = job;
   t_sync();
   ec_fork_begin(W::NT);
-  do_job(w, job, EC_TID, W::NT);
+  do_job(w, job, EC_TID_OF(W::NT), W::NT);
   ec_fork_end(W::NT);
 }
 
@@ -1044,7 +1053,7 @@ EC_DEV void helper_loop(W* w) {
     ec_fork_begin(W::NT);
     const int job = w->job;
     if (job == JOB_EXIT) break;
-    do_job(w, job, EC_TID, W::NT);
+    do_job(w, job, EC_TID_OF(W::NT), W::NT);
     ec_fork_end(W::NT);
   }
 }
@@ -1828,7 +1837,7 @@ EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
     }
     w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
   }
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   const double threshold = sc.consolidation_threshold * (double)sc.capacity;
   for (int k = tid >> 5; k < n_dep; k += nthr >> 5) {
     const int p = w->dep_pos[k];
@@ -2383,7 +2392,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
       const SKey k = skey_of(w, j, n_all); /* j >= n_all: (~0, ~0), sorts last */
       key[j] = make_ulonglong2(k.k1, k.k2);
     }
-    ec_team_barrier();
+    ec_team_barrier(W::NT);
     for (int k = 2; k <= N; k <<= 1) {
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
         for (int i = tid; i < N; i += nthr) {
@@ -2397,7 +2406,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
             }
           }
         }
-        ec_team_barrier();
+        ec_team_barrier(W::NT);
       }
     }
     for (int p = tid; p < n_all; p += nthr) {
@@ -2409,7 +2418,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     const SKey k = skey_of(w, j, n_all);
     key[j] = make_ulonglong2(k.k1, k.k2);
   }
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   for (int j = tid; j < n_all; j += nthr) {
     const ulonglong2 me = key[j];
     int rank = 0;
@@ -2429,7 +2438,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     emit(j, rank, me.x);
   }
   }
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   /* exact (time, prio) ties with an unknown push seq need the serial walk */
   int tie_unknown = 0;
   for (int p = tid + 1; p < n_all; p += nthr) {
@@ -2482,7 +2491,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     w->ks[j] = r.seq;
     w->ki[j] = (short)(empty || r.prio == EV_ARRIVAL ? 0 : r.inst);
   }
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   int tie_unknown = 0;
   for (int j = tid; j < n_all; j += nthr) {
     if (w->kp[j] == 0xff) continue;
@@ -2525,7 +2534,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (!below_horizon(tj, pj, sj, w->hz_t, (unsigned)w->hz_p, w->hz_s)) t_atomic_min_i(&w->j_cut, rank);
   }
   if (tie_unknown) w->j_tie_unknown = 1;
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   if (tid < EC_TSIZE) { /* warp 0: exclusive scan of the per-instance record counts */
     long long run = 0;
     for (int base = 0; base < M; base += EC_TSIZE) {
@@ -2537,7 +2546,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     }
     EC_LANE0 w->ioff[M] = (int)run;
   }
-  ec_team_barrier();
+  ec_team_barrier(W::NT);
   for (int j = tid; j < n_all; j += nthr) {
     const int ij = w->ki[j];
     if (ij && w->kp[j] != 0xff) w->ilist[w->ioff[ij - 1] + w->kir[j]] = w->krank[j];
@@ -2996,6 +3005,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     }
     t_sync();
     EC_DBG(0, k);
+    EC_EPOCH_SYNC(W::NT); /* lockstep builds: co-resident teams start each epoch together */
     epoch_event<W, DCAP>(w, g, k);
     EC_DBG(1, k);
     /* watchdog: every batch commits or executes at least one event, so a

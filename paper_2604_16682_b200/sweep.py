@@ -10,6 +10,11 @@ writes ``sweep.csv``.  Here the cells of a sweep run in ONE engine launch
     outcomes = run_cells(base, sweep_cells({"level_mhz": [660.0, 1680.0], "policy": ["round_robin"]}))
     write_sweep_table("out/sweep.csv", outcomes)
 
+Beyond the reference's four axes (config.py:64), ``capacity``, ``variant``
+and ``seed`` express the BASELINE sweeps: C3 is
+``{"level_mhz": 8 levels, "capacity": 4 caps, "seed": range(64)}`` and C5
+``{"slo_target": [20, 35], "policy": [...], "variant": [...], "seed": ...}``.
+
 A cell that fails validation is recorded with its error and the sweep
 continues (cli.py:172-174); the others still share the launch.  The YAML
 front end (``ExperimentConfig``) is out of scope, so cells apply to a
@@ -28,17 +33,25 @@ from .errors import ConfigurationError, SimulationError
 from .metrics import SUMMARY_FIELDS, format_value
 
 SWEEP_AXES = ("level_mhz", "arrival_rate", "slo_target", "policy")  # config.py:64
+# axes beyond the reference's four, for the BASELINE sweeps the reference CLI
+# cannot express (C3: seed x level x capacity; C5: seed x policy x variant x
+# SLO target).  They come after the reference's axes in the cell order and
+# the sweep.csv columns, so a sweep over the reference's axes alone is
+# unchanged.
+EXTRA_AXES = ("capacity", "variant", "seed")
+ALL_AXES = SWEEP_AXES + EXTRA_AXES
 
 
 def sweep_cells(axes: Mapping[str, Sequence]) -> list[dict]:
-    """Cartesian product of the given axes in SWEEP_AXES order (cli.py:136-158)."""
-    unknown = [a for a in axes if a not in SWEEP_AXES]
+    """Cartesian product of the given axes in ALL_AXES order (cli.py:136-158):
+    the last axis varies fastest."""
+    unknown = [a for a in axes if a not in ALL_AXES]
     if unknown:
         raise ConfigurationError(f"sweep: unknown axis {unknown[0]!r}")
     for axis, values in axes.items():
         if values is not None and not list(values):
             raise ConfigurationError(f"sweep.{axis}: axis must be non-empty")
-    names = [a for a in SWEEP_AXES if axes.get(a) is not None]
+    names = [a for a in ALL_AXES if axes.get(a) is not None]
     if not names:
         raise ConfigurationError("sweep: at least one non-empty axis is required")
     return [dict(zip(names, combo)) for combo in itertools.product(*(list(axes[n]) for n in names))]
@@ -57,6 +70,13 @@ def apply_cell(base: SimConfig, cell: Mapping) -> SimConfig:
         out = replace(out, controller=replace(out.controller, slo_target=float(cell["slo_target"])))
     if "policy" in cell:
         out = replace(out, router=replace(out.router, policy=str(cell["policy"]).replace("-", "_")))
+    if "capacity" in cell:
+        out = replace(out, instance=replace(out.instance, capacity_tokens=int(cell["capacity"])))
+    if "variant" in cell:
+        out = replace(out, controller=replace(out.controller, variant=str(cell["variant"]).replace("-", "_")))
+    if "seed" in cell:
+        # SimConfig.seed overrides the workload's seed (engine.py:70, 286-289)
+        out = replace(out, seed=int(cell["seed"]))
     return out
 
 
@@ -109,7 +129,7 @@ def run_cells(base: SimConfig, cells: Sequence[Mapping], *, device=None,
 def write_sweep_table(path: str, outcomes: Sequence[tuple[dict, dict | None, str | None]]) -> int:
     """``sweep.csv`` in the reference's format (cli.py:190-210); returns the
     number of failed cells."""
-    axis_names = [a for a in SWEEP_AXES if outcomes and a in outcomes[0][0]]
+    axis_names = [a for a in ALL_AXES if outcomes and a in outcomes[0][0]]
     header = axis_names + list(SUMMARY_FIELDS) + ["arrived", "completed", "status", "error"]
     failed = 0
     os.makedirs(os.path.dirname(os.path.abspath(path)), exist_ok=True)

@@ -49,10 +49,10 @@ static inline float ec_f32_down(double x) {
   return f;
 }
 #define EC_INF_F32 (__builtin_inff())
-#define EC_TID 0
+#define EC_TID_OF(nt) 0
 static inline void ec_fork_begin(int) {}
 static inline void ec_fork_end(int) {}
-static inline void ec_team_barrier() {}
+static inline void ec_team_barrier(int) {}
 static inline int t_atomic_min_i(int* p, int v) { int o = *p; if (v < o) *p = v; return o; }
 static inline unsigned long long t_warp_min_ull(unsigned long long v) { return v; }
 static inline void t_warp_min_key(unsigned long long&, unsigned&) {}

@@ -106,3 +106,33 @@ def test_gpu_sweep_csv_matches_reference_cli(cuda_device, tmp_path, name):
     path = tmp_path / "sweep.csv"
     assert sweep.write_sweep_table(str(path), outcomes) == 0
     assert path.read_text(encoding="utf-8") == case["sweep_csv"]
+
+
+def test_extra_axes_express_the_baseline_sweeps(tmp_path):
+    """seed / capacity / variant axes (beyond the reference's four): a
+    C3-shaped sweep (level x capacity x seed) through run_cells equals the
+    configs built by hand, and sweep.csv gets the extra columns last."""
+    table = asb.default_frequency_table(mhz=(660, 810, 900, 1035, 1185, 1350, 1515, 1680))
+    base = asb.SimConfig(workload=asb.WorkloadSpec(arrival_rate=0.1, duration=150.0, seed=0), sim_duration=200.0,
+                         instance=asb.InstanceConfig(frequency_table=table))
+    cells = sweep.sweep_cells({"seed": [3, 4], "level_mhz": [660.0, 1185.0], "capacity": [20_000, 60_000]})
+    assert len(cells) == 8 and list(cells[0]) == ["level_mhz", "capacity", "seed"]
+    assert [c["seed"] for c in cells[:2]] == [3, 4]  # the last axis varies fastest
+    cfgs = [sweep.apply_cell(base, c) for c in cells]
+    assert cfgs[1].seed == 4 and cfgs[2].instance.capacity_tokens == 60_000
+    assert cfgs[0].controller.variant == "fixed" and cfgs[0].controller.fixed_level_mhz == 660.0
+    outcomes = sweep.run_cells(base, cells, runner=oracle_runner)
+    by_hand = [asb.SimConfig(workload=asb.WorkloadSpec(arrival_rate=0.1, duration=150.0, seed=c["seed"]),
+                             sim_duration=200.0,
+                             instance=asb.InstanceConfig(capacity_tokens=c["capacity"], frequency_table=table),
+                             controller=asb.ControllerConfig(variant="fixed", fixed_level_mhz=c["level_mhz"]))
+               for c in cells]
+    for (cell, summary, err), r in zip(outcomes, oracle_runner(by_hand)):
+        assert err is None and summary["energy"] == r.system.energy and summary["completed"] == r.completed
+    sweep.write_sweep_table(str(tmp_path / "sweep.csv"), outcomes)
+    header = (tmp_path / "sweep.csv").read_text().splitlines()[0].split(",")
+    assert header[:2] == ["level_mhz", "capacity"] and header[2] == "seed"
+    v = sweep.sweep_cells({"variant": ["off", "context-aware"], "policy": ["round-robin"]})
+    assert sweep.apply_cell(base, v[1]).controller.variant == "context_aware"
+    with pytest.raises(asb.ConfigurationError, match="unknown axis"):
+        sweep.sweep_cells({"seeds": [1]})

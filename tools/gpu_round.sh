@@ -17,4 +17,6 @@ echo done
 # the other BASELINE configs (reported in DESIGN.md; the driver's headline is c5)
 timeout 900 python bench.py --config c3 --steps 3 --warmup 3 > $OUT/bench_c3.json 2> $OUT/bench_c3.err
 timeout 900 python bench.py --config c4 --steps 3 --warmup 3 > $OUT/bench_c4.json 2> $OUT/bench_c4.err
+timeout 900 python bench.py --config c5full --steps 3 --warmup 3 --no-cpu-baseline > $OUT/bench_c5full.json 2> $OUT/bench_c5full.err
+timeout 900 python tools/time_batch_api.py 64 $OUT/batch_api.json > $OUT/batch_api.log 2>&1
 echo done2

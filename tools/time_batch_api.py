@@ -22,10 +22,10 @@ from paper_2604_16682_b200.engine import BatchResult, DeviceBatch, build_results
 
 def main():
     seeds = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-    cells = bench.c5_cells()
-    cfgs = [asb.SimConfig(workload=bench.workload_spec("c5", s), instance_count=c.instance_count,
-                          sim_duration=c.sim_duration, controller=c.controller, router=c.router)
-            for s in range(seeds) for c in cells]
+    from paper_2604_16682_b200 import sweep
+
+    base = bench.base_config("c5")
+    cfgs = [sweep.apply_cell(base, c) for c in sweep.sweep_cells(bench.sweep_axes("c5", list(range(seeds))))]
     out = {"scenarios": len(cfgs)}
     t0 = time.perf_counter()
     batch = prepare_batch(cfgs)
