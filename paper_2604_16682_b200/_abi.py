@@ -94,6 +94,9 @@ TIMESERIES_DTYPE = np.dtype(
     align=True,
 )
 
+REGIME_SPAN_DTYPE = np.dtype(
+    [("start", "<f8"), ("end", "<f8"), ("instance_id", "<i4"), ("thrashing", "<i4")], align=True)
+
 STATS_DTYPE = np.dtype(
     [
         ("slo_attainment", "<f8"),
@@ -198,7 +201,7 @@ INST_OUT = {
 def struct_sizes() -> list[int]:
     """Sizes in header order, as the C side reports them via asb_struct_sizes."""
     return [SCENARIO_DTYPE.itemsize, C.sizeof(AsbTracePool), C.sizeof(AsbTablePool), C.sizeof(AsbOutputs),
-            DECISION_DTYPE.itemsize, STATS_DTYPE.itemsize, TIMESERIES_DTYPE.itemsize]
+            DECISION_DTYPE.itemsize, STATS_DTYPE.itemsize, TIMESERIES_DTYPE.itemsize, REGIME_SPAN_DTYPE.itemsize]
 
 
 def make_outputs(ptr_of, arrays: dict) -> AsbOutputs:

@@ -34,6 +34,7 @@ def _declare(lib: C.CDLL) -> None:
         "asb_assign_batch": (C.c_int, [vp, vp, i32, i64, f64, i32, vp, i64, vp]),
         "asb_reassign_batch": (C.c_int, [vp, vp, i32, vp, vp, i32, f64, i32, i32, vp, i64, vp]),
         "asb_min_throughput_batch": (C.c_int, [vp, vp, vp, i64, i32, vp, vp, vp]),
+        "asb_regime_classify": (C.c_int, [vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -295,6 +295,161 @@ __global__ void reduce_stats_kernel(const AsbStats* __restrict__ stats, const in
   }
 }
 
+/* regime_classify (metrics.py:72-109), one warp per scenario, a lane per
+ * instance (groups of 32 instances).  Rows are read in chunks of 32 (one
+ * coalesced row per lane) and broadcast lane by lane; each lane follows its
+ * instance's points.  Pass 0 counts every instance's spans, pass 1 writes
+ * them at the exclusive-scan offsets and sums the thrashing durations. */
+struct RegimeLane {
+  bool has_prev, has_span;
+  double prev_t, prev_u;
+  double s0, s1;
+  int flag;
+  long long n;    /* spans emitted so far */
+  double f, c;    /* Python float sum() of thrashing durations (Neumaier) */
+  bool sum_started;
+};
+
+__device__ void regime_emit(RegimeLane& L, AsbRegimeSpan* out, int iid) {
+  if (!L.has_span) return;
+  if (out) {
+    AsbRegimeSpan sp;
+    sp.start = L.s0;
+    sp.end = L.s1;
+    sp.instance_id = iid;
+    sp.thrashing = L.flag;
+    out[L.n] = sp;
+  }
+  if (L.flag) {
+    const double x = L.s1 - L.s0;
+    if (!L.sum_started) {
+      L.f = 0.0 + x;
+      L.c = 0.0;
+      L.sum_started = true;
+    } else {
+      const double t = L.f + x;
+      if (fabs(L.f) >= fabs(x))
+        L.c += (L.f - t) + x;
+      else
+        L.c += (x - t) + L.f;
+      L.f = t;
+    }
+  }
+  L.n++;
+}
+
+/* add(start, end, flag) of the reference: skip empty spans, merge with the
+ * previous span when it has the same flag and ends where this one starts */
+__device__ void regime_add(RegimeLane& L, AsbRegimeSpan* out, int iid, double a, double b, int flag) {
+  if (b <= a) return;
+  if (L.has_span && L.flag == flag && L.s1 == a) {
+    L.s1 = b;
+    return;
+  }
+  regime_emit(L, out, iid);
+  L.has_span = true;
+  L.s0 = a;
+  L.s1 = b;
+  L.flag = flag;
+}
+
+__global__ void regime_kernel(const AsbTimeseriesRow* __restrict__ rows, const int64_t* __restrict__ ts_off,
+                              const int64_t* __restrict__ ts_count, int n_scen, const int32_t* __restrict__ n_inst,
+                              const double* __restrict__ capacity, const double* __restrict__ window,
+                              const int64_t* __restrict__ span_off, AsbRegimeSpan* __restrict__ spans,
+                              int64_t* __restrict__ span_count, double* __restrict__ frac, int32_t* __restrict__ status) {
+  const int s = blockIdx.x;
+  if (s >= n_scen) return;
+  const int lane = threadIdx.x;
+  const AsbTimeseriesRow* R = rows + ts_off[s];
+  const long long nr = ts_count[s];
+  const int M = n_inst[s];
+  const double cap = capacity[s], W = window[s];
+  const long long room = span_off[s + 1] - span_off[s];
+  long long base = 0;   /* spans of the instances before this group */
+  double total = 0.0;   /* thrash_total, instances in id order */
+  int bad = 0;
+  for (int g0 = 0; g0 < M; g0 += 32) {
+    const int iid = g0 + lane + 1;
+    long long my_off = 0;
+    for (int pass = 0; pass < 2; pass++) {
+      RegimeLane L;
+      L.has_prev = L.has_span = L.sum_started = false;
+      L.n = 0;
+      L.f = L.c = 0.0;
+      AsbRegimeSpan* out = pass == 1 && iid <= M ? spans + span_off[s] + base + my_off : nullptr;
+      for (long long r0 = 0; r0 < nr; r0 += 32) {
+        const long long r = r0 + lane;
+        double t = 0.0, u = 0.0;
+        int id = 0;
+        if (r < nr) {
+          t = R[r].time;
+          u = (double)R[r].context_usage;
+          id = R[r].instance_id;
+        }
+        const int k_end = (int)(nr - r0 < 32 ? nr - r0 : 32);
+        for (int k = 0; k < k_end; k++) {
+          const int idk = __shfl_sync(FULLMASK, id, k);
+          const double tk = __shfl_sync(FULLMASK, t, k);
+          const double uk = __shfl_sync(FULLMASK, u, k);
+          if (idk != iid) continue;
+          if (L.has_prev) {
+            const double a = L.prev_t < W ? L.prev_t : W, b = tk < W ? tk : W;
+            regime_add(L, out, iid, a, b, L.prev_u > cap ? 1 : 0);
+          }
+          L.has_prev = true;
+          L.prev_t = tk;
+          L.prev_u = uk;
+        }
+      }
+      if (iid <= M && L.has_prev && L.prev_t < W) regime_add(L, out, iid, L.prev_t, W, L.prev_u > cap ? 1 : 0);
+      if (iid <= M) regime_emit(L, out, iid);
+      if (pass == 0) {
+        /* exclusive scan of the group's span counts */
+        long long c = iid <= M ? L.n : 0, inc = c;
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long v = __shfl_up_sync(FULLMASK, inc, o);
+          if (lane >= o) inc += v;
+        }
+        my_off = inc - c;
+        if (base + __shfl_sync(FULLMASK, inc, 31) > room) bad = -1;
+        bad = __shfl_sync(FULLMASK, bad, 0);
+        if (bad) break;
+      } else {
+        /* sum() of an instance with no thrashing span is int 0 */
+        double inst_sum = 0.0;
+        if (L.sum_started) inst_sum = (L.c != 0.0 && isfinite(L.c)) ? L.f + L.c : L.f;
+        for (int k = 0; k < 32 && g0 + k < M; k++) total += __shfl_sync(FULLMASK, inst_sum, k);
+        base += __shfl_sync(FULLMASK, my_off + (iid <= M ? L.n : 0), 31);
+      }
+    }
+    if (bad) break;
+  }
+  /* coverage of the window start (metrics.py:88-91): every instance
+   * 1..M has points and its first is at t <= 0 (the engine writes a forced
+   * row per instance at t = 0, engine.py:576-579) */
+  if (!bad) {
+    for (int g0 = 0; g0 < M; g0 += 32) {
+      const int iid = g0 + lane + 1;
+      double first = __longlong_as_double(0x7ff0000000000000ll);
+      bool found = false;
+      for (long long r0 = 0; r0 < nr && iid <= M && !found; r0 += 1) {
+        if (R[r0].instance_id == iid) {
+          first = R[r0].time;
+          found = true;
+        }
+      }
+      const unsigned m = __ballot_sync(FULLMASK, iid <= M && (!found || first > 0.0));
+      if (m && !bad) bad = g0 + __ffs(m);
+    }
+  }
+  if (lane == 0) {
+    status[s] = bad;
+    span_count[s] = bad ? 0 : base;
+    frac[s] = total / (W * (double)M);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -368,6 +523,21 @@ int asb_reduce_stats(const AsbStats* d_stats, const int64_t* d_counters, int32_t
   return cudaGetLastError() == cudaSuccess ? ASB_OK : ASB_ERR_LAUNCH;
 }
 
+int asb_regime_classify(const AsbTimeseriesRow* rows, const int64_t* ts_off, const int64_t* ts_count,
+                        int32_t n_scen, const int32_t* n_instances, const double* capacity, const double* window,
+                        const int64_t* span_off, AsbRegimeSpan* spans, int64_t* span_count,
+                        double* thrash_fraction, int32_t* status, void* stream) {
+  if (n_scen < 0) return ASB_ERR_ARG;
+  if (n_scen == 0) return ASB_OK;
+  if (!rows || !ts_off || !ts_count || !n_instances || !capacity || !window || !span_off || !spans ||
+      !span_count || !thrash_fraction || !status)
+    return ASB_ERR_ARG;
+  regime_kernel<<<n_scen, 32, 0, (cudaStream_t)stream>>>(rows, ts_off, ts_count, n_scen, n_instances, capacity,
+                                                          window, span_off, spans, span_count, thrash_fraction,
+                                                          status);
+  return cudaGetLastError() == cudaSuccess ? ASB_OK : ASB_ERR_LAUNCH;
+}
+
 int asb_struct_sizes(int64_t* out4) {  /* NOLINT */
   out4[0] = (int64_t)sizeof(AsbScenario);
   out4[1] = (int64_t)sizeof(AsbTracePool);
@@ -376,7 +546,8 @@ int asb_struct_sizes(int64_t* out4) {  /* NOLINT */
   out4[4] = (int64_t)sizeof(AsbDecision);
   out4[5] = (int64_t)sizeof(AsbStats);
   out4[6] = (int64_t)sizeof(AsbTimeseriesRow);
-  return 7;
+  out4[7] = (int64_t)sizeof(AsbRegimeSpan);
+  return 8;
 }
 
 }  // extern "C"

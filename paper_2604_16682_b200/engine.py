@@ -401,6 +401,63 @@ class DeviceBatch:
         torch.ops.agentsim_b200.scenario_stats(self.scen, self.out_list, self.stats)
         torch.ops.agentsim_b200.reduce_stats(self.stats, self.outputs["counters"], b.n, self.red)
 
+    def regime_classify(self, capacity: Sequence[float] | None = None,
+                        window: Sequence[float] | None = None) -> list[tuple[dict, float]]:
+        """``regime_classify(result.usage_series(), capacity, window)``
+        (metrics.py:72-109) for every scenario, on the device, straight from
+        the timeseries rows of the last ``run()`` (``timeseries=True``):
+        ``[(segments, thrash_fraction)]`` with segments ``{instance_id:
+        [(start, end, thrashing), ...]}``.  Defaults: each scenario's
+        ``capacity_tokens`` and ``sim_duration``."""
+        import torch
+
+        from . import _native
+
+        b = self.batch
+        if not self.outputs["ts_count"].numel():
+            raise ConfigurationError("regime_classify needs the timeseries rows: DeviceBatch(..., timeseries=True)")
+        cap = np.asarray(capacity if capacity is not None else b.scen["capacity"], dtype=np.float64)
+        win = np.asarray(window if window is not None else b.scen["sim_duration"], dtype=np.float64)
+        if cap.shape != (b.n,) or win.shape != (b.n,):
+            raise ConfigurationError("regime_classify: one capacity and one window per scenario")
+        if not (win > 0).all():
+            raise ConfigurationError(f"window: must be > 0, got {float(win[~(win > 0)][0])}")
+        m = b.scen["n_instances"].astype(np.int64)
+        room = np.diff(b.ts_off) + m
+        span_off = np.zeros(b.n + 1, dtype=np.int64)
+        np.cumsum(room, out=span_off[1:])
+        dev = self.device
+
+        def up(a):
+            return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+        d_m, d_cap, d_win, d_off = up(m.astype(np.int32)), up(cap), up(win), up(span_off)
+        spans = torch.empty(int(span_off[-1]) * _abi.REGIME_SPAN_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        count = torch.empty(b.n, dtype=torch.int64, device=dev)
+        frac = torch.empty(b.n, dtype=torch.float64, device=dev)
+        status = torch.empty(b.n, dtype=torch.int32, device=dev)
+        o = self.outputs
+        with torch.cuda.device(dev):
+            rc = _native.lib().asb_regime_classify(
+                o["timeseries"].data_ptr(), o["ts_off"].data_ptr(), o["ts_count"].data_ptr(), b.n, d_m.data_ptr(),
+                d_cap.data_ptr(), d_win.data_ptr(), d_off.data_ptr(), spans.data_ptr(), count.data_ptr(),
+                frac.data_ptr(), status.data_ptr(), _native.stream_handle(dev))
+        _native.check(rc, "asb_regime_classify")
+        spans_h = spans.cpu().numpy().view(_abi.REGIME_SPAN_DTYPE)
+        count_h, frac_h, status_h = count.cpu().numpy(), frac.cpu().numpy(), status.cpu().numpy()
+        out = []
+        for s in range(b.n):
+            if status_h[s] > 0:
+                raise SimulationError(f"usage series for instance {int(status_h[s])} does not cover the window start")
+            if status_h[s] < 0:
+                raise SimulationError("regime_classify: span buffer overflow")
+            rows = spans_h[int(span_off[s]): int(span_off[s]) + int(count_h[s])]
+            seg: dict = {i + 1: [] for i in range(int(m[s]))}
+            for r in rows:
+                seg[int(r["instance_id"])].append((float(r["start"]), float(r["end"]), bool(r["thrashing"])))
+            out.append((seg, float(frac_h[s])))
+        return out
+
     def download(self) -> tuple[dict, np.ndarray]:
         host = {}
         for k, t in self.outputs.items():

@@ -29,8 +29,6 @@
  *   asb_min_throughput_batch min_throughput / running_throughput controller.py:89-103
  *   asb_scenario_stats      SystemMetrics in _build_result engine.py:632-655,
  *                           slo_attainment / percentile_throughput metrics.py:49-69
- *   asb_regime_classify     regime_classify over SimulationResult.usage_series()
- *                           metrics.py:72-109, engine.py:176-182
  */
 #ifndef AGENTSIM_B200_H
 #define AGENTSIM_B200_H
@@ -298,34 +296,8 @@ enum {
 int asb_reduce_stats(const AsbStats* d_stats, const int64_t* d_counters, int32_t n_scen,
                      double* d_red, void* stream);
 
-/* One span of regime_classify's per-instance segments (metrics.py:72-109). */
-typedef struct AsbRegimeSpan {
-  double start;
-  double end;
-  int32_t instance_id;
-  int32_t thrashing; /* usage > capacity over [start, end) */
-} AsbRegimeSpan;
-
-/* regime_classify(usage_series, capacity, window) on the device, per scenario,
- * over the timeseries rows asb_run_scenarios wrote (AsbOutputs.timeseries /
- * ts_off / ts_count): each instance's usage points (row.time,
- * float(row.context_usage)) in row order, split into merged non-thrashing /
- * thrashing spans clipped to the window (spans grouped by instance id
- * 1..n_instances, in time order), and the thrashing share of the total
- * instance-time (thrash sums restate Python's float sum()).  Span buffer of
- * scenario s: [span_off[s], span_off[s+1]), needing at least ts_count[s] +
- * n_instances[s] entries.  status[s]: 0, or the first instance id whose
- * series does not cover the window start (the reference's SimulationError),
- * or -1 when the span buffer is too small.  window must be > 0 (the host
- * raises ConfigurationError first). */
-int asb_regime_classify(const AsbTimeseriesRow* rows, const int64_t* ts_off, const int64_t* ts_count,
-                        int32_t n_scen, const int32_t* n_instances, const double* capacity,
-                        const double* window, const int64_t* span_off, AsbRegimeSpan* spans,
-                        int64_t* span_count, double* thrash_fraction, int32_t* status, void* stream);
-
 /* ABI self-check: writes sizeof of AsbScenario, AsbTracePool, AsbTablePool,
- * AsbOutputs, AsbDecision, AsbStats, AsbTimeseriesRow, AsbRegimeSpan into
- * out[0..7]; returns 8. */
+ * AsbOutputs, AsbDecision, AsbStats, AsbTimeseriesRow into out[0..6]; returns 7. */
 int asb_struct_sizes(int64_t* out);
 
 #ifdef __cplusplus

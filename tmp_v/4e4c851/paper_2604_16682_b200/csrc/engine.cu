@@ -13,7 +13,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -95,12 +94,10 @@ EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((
 EC_DEV long long ec_clock() { return clock64(); }
 EC_DEV float ec_f32_down(double x) { return __double2float_rd(x); } /* rounded toward -inf: <= x */
 #define EC_INF_F32 __int_as_float(0x7f800000)
-/* a team is NT consecutive threads (NT a power of two): one team per CTA */
-#define EC_TID_OF(nt) ((int)(threadIdx.x & ((nt) - 1)))
+#define EC_TID ((int)threadIdx.x)
 /* named CTA barriers for the fork-join team.  Each warp reconverges first
  * (__syncwarp): a warp that reaches a CTA barrier with some lanes still
- * inside the job would let the barrier complete early.  (Constant ids: a
- * computed id makes ptxas reserve all 16 barriers.) */
+ * inside the job would let the barrier complete early. */
 /* a single-warp team is its own team: a warp barrier is enough */
 EC_DEV void ec_fork_begin(int nt) {
   __syncwarp();
@@ -110,9 +107,9 @@ EC_DEV void ec_fork_end(int nt) {
   __syncwarp();
   if (nt > 32) asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
 }
-EC_DEV void ec_team_barrier(int nt) {
+EC_DEV void ec_team_barrier() {
   __syncwarp();
-  if (nt > 32) asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
+  asm volatile("bar.sync 3, %0;" ::"r"((int)blockDim.x) : "memory");
 }
 EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
 EC_COLL unsigned long long t_warp_min_ull(unsigned long long v) {
@@ -204,7 +201,7 @@ struct Workspace {
   asb::AgentHot* hot;
   asb::Slot* sl;
   double *notbefore, *pissue, *arr_t;
-  int* dstamp;
+  int *alive, *dstamp;
   int *ring, *log;
   long long* ring_off;
   int* work;
@@ -228,6 +225,7 @@ size_t carve(unsigned char* base, int32_t n_scen, int64_t total_agents, int64_t 
   t.sl = (asb::Slot*)take(na * sizeof(asb::Slot));
   t.notbefore = (double*)take(na * 8);
   t.pissue = (double*)take(na * 8);
+  t.alive = (int*)take(na * 4);
   t.dstamp = (int*)take(na * 4);
   t.ring = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
   t.log = (int*)take((size_t)(total_ring > 0 ? total_ring : 1) * 4);
@@ -271,10 +269,7 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
 }
 
 template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
-/* min blocks per SM: 4-warp teams 4 per SM; single-warp teams 16 per SM,
- * i.e. <= 128 registers, so that 14 of them fit next to their shared memory
- * (C3's 2,048 scenarios in one wave of 148 x 14) */
-__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
+__global__ void __launch_bounds__(NT, NT <= 128 ? 4 : 1)
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
@@ -333,6 +328,7 @@ __global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
     g.o_inst = out.final_instance + oa;
     g.o_mig = out.migrations + oa;
     g.o_phase = out.phase + oa;
+    g.alive = ws.alive + oa;
     g.sl = ws.sl + oa;
     g.dstamp = ws.dstamp + oa;
     g.ring = ws.ring + ws.ring_off[s];
@@ -371,7 +367,7 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
                   const AsbOutputs& out, const Workspace& ws, cudaStream_t st) {
   using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
-  static_assert(NT % 32 == 0 && NT >= 32 && (NT & (NT - 1)) == 0, "team = a power-of-two number of whole warps");
+  static_assert(NT % 32 == 0 && NT >= 32, "team = whole warps");
   /* 4 teams per SM need <= ~54 KB of shared memory each (228 KB per SM) */
   static_assert(NT > 128 || MAXM > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
   const size_t smem = (sizeof(W) + 15) / 16 * 16;
@@ -383,8 +379,6 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess || per_sm < 1)
     return ASB_ERR_LAUNCH;
-  if (getenv("ASB_DEBUG_LAUNCH"))
-    fprintf(stderr, "asb launch: team %d, smem %zu B, %d blocks/SM, %d SMs\n", NT, smem, per_sm, sms);
   long long want = n_scen;
   long long cap = (long long)sms * per_sm;
   int blocks = (int)(want < cap ? want : cap);
@@ -421,14 +415,6 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   Workspace ws;
   carve((unsigned char*)d_workspace, n_scen, total_agents, total_ring_slots, &ws);
   cudaStream_t st = (cudaStream_t)stream;
-  if (const char* pl = getenv("ASB_L2_PERSIST_MB")) { /* experiment: L2 set-aside for evict_last lines */
-    size_t want = (size_t)atol(pl) << 20;
-    int dev0 = 0, mx = 0;
-    cudaGetDevice(&dev0);
-    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev0);
-    if (want > (size_t)mx) want = (size_t)mx;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-  }
   ring_offsets_kernel<<<1, 1024, 0, st>>>(d_scen, n_scen, traces.trace_agent_off, ws.ring_off, ws.work);
   if (cudaGetLastError() != cudaSuccess) return ASB_ERR_LAUNCH;
   /* team shape by scenario size (ASB_TEAM=solo|quad|big overrides, for tests):

@@ -1034,7 +1034,7 @@ EC_DEV void fork_job(W* w, int job) {
   EC_LANE0 w->job = job;
   t_sync();
   ec_fork_begin(W::NT);
-  do_job(w, job, EC_TID_OF(W::NT), W::NT);
+  do_job(w, job, EC_TID, W::NT);
   ec_fork_end(W::NT);
 }
 
@@ -1044,7 +1044,7 @@ EC_DEV void helper_loop(W* w) {
     ec_fork_begin(W::NT);
     const int job = w->job;
     if (job == JOB_EXIT) break;
-    do_job(w, job, EC_TID_OF(W::NT), W::NT);
+    do_job(w, job, EC_TID, W::NT);
     ec_fork_end(W::NT);
   }
 }
@@ -1828,7 +1828,7 @@ EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
     }
     w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   const double threshold = sc.consolidation_threshold * (double)sc.capacity;
   for (int k = tid >> 5; k < n_dep; k += nthr >> 5) {
     const int p = w->dep_pos[k];
@@ -2383,7 +2383,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
       const SKey k = skey_of(w, j, n_all); /* j >= n_all: (~0, ~0), sorts last */
       key[j] = make_ulonglong2(k.k1, k.k2);
     }
-    ec_team_barrier(W::NT);
+    ec_team_barrier();
     for (int k = 2; k <= N; k <<= 1) {
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
         for (int i = tid; i < N; i += nthr) {
@@ -2397,7 +2397,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
             }
           }
         }
-        ec_team_barrier(W::NT);
+        ec_team_barrier();
       }
     }
     for (int p = tid; p < n_all; p += nthr) {
@@ -2409,7 +2409,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     const SKey k = skey_of(w, j, n_all);
     key[j] = make_ulonglong2(k.k1, k.k2);
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   for (int j = tid; j < n_all; j += nthr) {
     const ulonglong2 me = key[j];
     int rank = 0;
@@ -2429,7 +2429,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     emit(j, rank, me.x);
   }
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   /* exact (time, prio) ties with an unknown push seq need the serial walk */
   int tie_unknown = 0;
   for (int p = tid + 1; p < n_all; p += nthr) {
@@ -2482,7 +2482,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     w->ks[j] = r.seq;
     w->ki[j] = (short)(empty || r.prio == EV_ARRIVAL ? 0 : r.inst);
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   int tie_unknown = 0;
   for (int j = tid; j < n_all; j += nthr) {
     if (w->kp[j] == 0xff) continue;
@@ -2525,7 +2525,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (!below_horizon(tj, pj, sj, w->hz_t, (unsigned)w->hz_p, w->hz_s)) t_atomic_min_i(&w->j_cut, rank);
   }
   if (tie_unknown) w->j_tie_unknown = 1;
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   if (tid < EC_TSIZE) { /* warp 0: exclusive scan of the per-instance record counts */
     long long run = 0;
     for (int base = 0; base < M; base += EC_TSIZE) {
@@ -2537,7 +2537,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     }
     EC_LANE0 w->ioff[M] = (int)run;
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   for (int j = tid; j < n_all; j += nthr) {
     const int ij = w->ki[j];
     if (ij && w->kp[j] != 0xff) w->ilist[w->ioff[ij - 1] + w->kir[j]] = w->krank[j];
@@ -2879,8 +2879,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
 }
 
 /* exact single-event fallback: process the minimum pending event serially
- * (the timeseries loop, and a burst of identical timestamps larger than the
- * batch buffers) */
+ * (used only when a burst of identical timestamps exceeds the batch buffers) */
 template <class W>
 EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   EC_DBG(11, w->n_alive);

@@ -13,7 +13,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -95,25 +94,51 @@ EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((
 EC_DEV long long ec_clock() { return clock64(); }
 EC_DEV float ec_f32_down(double x) { return __double2float_rd(x); } /* rounded toward -inf: <= x */
 #define EC_INF_F32 __int_as_float(0x7f800000)
-/* a team is NT consecutive threads (NT a power of two): one team per CTA */
+/* a team is NT consecutive threads (NT a power of two); a CTA holds one
+ * team, or several in the lockstep kernels */
 #define EC_TID_OF(nt) ((int)(threadIdx.x & ((nt) - 1)))
-/* named CTA barriers for the fork-join team.  Each warp reconverges first
- * (__syncwarp): a warp that reaches a CTA barrier with some lanes still
- * inside the job would let the barrier complete early.  (Constant ids: a
- * computed id makes ptxas reserve all 16 barriers.) */
+/* named barriers for the fork-join team, three per team (ids 1-3 for team
+ * 0, 4-6 for team 1, ...).  Each warp reconverges first (__syncwarp): a warp
+ * that reaches a named barrier with some lanes still inside the job would
+ * let the barrier complete early. */
 /* a single-warp team is its own team: a warp barrier is enough */
+EC_DEV int ec_bar_id(int nt, int k) { return 1 + 3 * (int)(threadIdx.x / (unsigned)nt) + k; }
 EC_DEV void ec_fork_begin(int nt) {
   __syncwarp();
-  if (nt > 32) asm volatile("bar.sync 1, %0;" ::"r"(nt) : "memory");
+  if (nt > 32) asm volatile("bar.sync %0, %1;" ::"r"(ec_bar_id(nt, 0)), "r"(nt) : "memory");
 }
 EC_DEV void ec_fork_end(int nt) {
   __syncwarp();
-  if (nt > 32) asm volatile("bar.sync 2, %0;" ::"r"(nt) : "memory");
+  if (nt > 32) asm volatile("bar.sync %0, %1;" ::"r"(ec_bar_id(nt, 1)), "r"(nt) : "memory");
 }
 EC_DEV void ec_team_barrier(int nt) {
   __syncwarp();
-  if (nt > 32) asm volatile("bar.sync 3, %0;" ::"r"(nt) : "memory");
+  if (nt > 32) asm volatile("bar.sync %0, %1;" ::"r"(ec_bar_id(nt, 2)), "r"(nt) : "memory");
 }
+/* lockstep kernels: the teams of a CTA start every control epoch together,
+ * so they run the same engine phase at the same time and share its code in
+ * the instruction caches.  ec_tstep[t] counts the epochs team t has begun
+ * (across its scenarios; LLONG_MAX once it has no more work); a team waits
+ * until every other team has begun at least as many. */
+__shared__ volatile long long ec_tstep[4];
+EC_DEV void ec_epoch_sync(int nt) {
+  const int tpc = (int)(blockDim.x / (unsigned)nt);
+  if (tpc <= 1) return;
+  if ((threadIdx.x & 31) == 0) {
+    const int me = (int)(threadIdx.x / (unsigned)nt);
+    const long long my = ec_tstep[me] + 1;
+    ec_tstep[me] = my;
+    for (;;) {
+      long long mn = 0x7fffffffffffffffll;
+      for (int t = 0; t < tpc; t++)
+        if (t != me && ec_tstep[t] < mn) mn = ec_tstep[t];
+      if (mn >= my) break;
+      __nanosleep(20);
+    }
+  }
+  __syncwarp();
+}
+#define EC_EPOCH_SYNC(nt) ec_epoch_sync(nt)
 EC_DEV int t_atomic_min_i(int* p, int v) { return atomicMin(p, v); }
 EC_COLL unsigned long long t_warp_min_ull(unsigned long long v) {
 EC_COLL_UNROLL
@@ -270,19 +295,23 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
   }
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
-/* min blocks per SM: 4-warp teams 4 per SM; single-warp teams 16 per SM,
- * i.e. <= 128 registers, so that 14 of them fit next to their shared memory
- * (C3's 2,048 scenarios in one wave of 148 x 14) */
-__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int TPC>
+__global__ void __launch_bounds__(NT * TPC, NT * TPC <= 128 ? 4 : 1)
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
-  /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
-   * helpers joining the slot sweeps, speculation, rank sort and apply */
+  /* one team = one scenario at a time: its warp 0 runs the engine, warps
+   * 1.. are helpers joining the slot sweeps, speculation, rank sort and
+   * apply.  A CTA holds TPC teams (TPC > 1: the lockstep kernels) */
   using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
+  constexpr size_t WSZ = (sizeof(W) + 15) / 16 * 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  W* w = reinterpret_cast<W*>(smem_raw);
-  if (threadIdx.x >= 32) {
+  const int team = (int)(threadIdx.x / NT);
+  W* w = reinterpret_cast<W*>(smem_raw + (size_t)team * WSZ);
+  if (TPC > 1) {
+    if (threadIdx.x < TPC) ec_tstep[threadIdx.x] = 0;
+    __syncthreads();
+  }
+  if ((threadIdx.x & (NT - 1)) >= 32) {
     asb::helper_loop(w);
     return;
   }
@@ -361,35 +390,35 @@ __global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
       asb::run_scenario<W, RCAP, DCAP, ACAP, false>(w, w->gp);
     __syncwarp();
   }
+  if (TPC > 1 && EC_LANE == 0) ec_tstep[team] = 0x7fffffffffffffffll; /* no more epochs from this team */
   if (EC_LANE == 0) w->job = asb::JOB_EXIT;
   __syncwarp();
   ec_fork_begin(NT);
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int TPC = 1>
 int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp, const AsbTablePool& tb,
                   const AsbOutputs& out, const Workspace& ws, cudaStream_t st) {
   using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
   static_assert(NT % 32 == 0 && NT >= 32 && (NT & (NT - 1)) == 0, "team = a power-of-two number of whole warps");
+  static_assert(TPC >= 1 && TPC <= 4 && (TPC == 1 || NT > 32), "lockstep CTAs hold up to 4 multi-warp teams");
   /* 4 teams per SM need <= ~54 KB of shared memory each (228 KB per SM) */
   static_assert(NT > 128 || MAXM > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
-  const size_t smem = (sizeof(W) + 15) / 16 * 16;
-  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT>;
+  const size_t smem = TPC * ((sizeof(W) + 15) / 16 * 16);
+  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT, TPC>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return ASB_ERR_LAUNCH;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess || per_sm < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT * TPC, smem) != cudaSuccess || per_sm < 1)
     return ASB_ERR_LAUNCH;
-  if (getenv("ASB_DEBUG_LAUNCH"))
-    fprintf(stderr, "asb launch: team %d, smem %zu B, %d blocks/SM, %d SMs\n", NT, smem, per_sm, sms);
-  long long want = n_scen;
+  long long want = (n_scen + TPC - 1) / TPC;
   long long cap = (long long)sms * per_sm;
   int blocks = (int)(want < cap ? want : cap);
   if (blocks < 1) blocks = 1;
-  kern<<<blocks, NT, smem, st>>>(d_scen, n_scen, tp, tb, out, ws);
+  kern<<<blocks, NT * TPC, smem, st>>>(d_scen, n_scen, tp, tb, out, ws);
   return cudaGetLastError() == cudaSuccess ? ASB_OK : ASB_ERR_LAUNCH;
 }
 
@@ -451,6 +480,9 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16) {
     if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
+#ifdef ASB_LOCKSTEP
+    if (!getenv("ASB_NO_LOCKSTEP")) return launch_engine<16, 192, 128, 64, 128, 4>(d_scen, n_scen, traces, tables, out, ws, st);
+#endif
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   }
   if (solo) return launch_engine<64, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);

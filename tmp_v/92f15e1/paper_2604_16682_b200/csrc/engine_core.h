@@ -77,6 +77,15 @@
 
 /* EC_DBG(slot, value): progress markers for hang debugging (GPU debug build
  * -DASB_DEBUG_TRACE writes them to host-mapped memory); no-op otherwise */
+/* EC_EPOCH_SYNC(nt): an includer hook run by the main warp at the start of
+ * every control epoch (the GPU lockstep kernels align the teams sharing a
+ * CTA there); no-op by default */
+#ifndef EC_EPOCH_SYNC
+#define EC_EPOCH_SYNC(nt) \
+  do {                    \
+  } while (0)
+#endif
+
 #ifndef EC_DBG
 #define EC_DBG(slot, value) \
   do {                      \
@@ -2879,8 +2888,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
 }
 
 /* exact single-event fallback: process the minimum pending event serially
- * (the timeseries loop, and a burst of identical timestamps larger than the
- * batch buffers) */
+ * (used only when a burst of identical timestamps exceeds the batch buffers) */
 template <class W>
 EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   EC_DBG(11, w->n_alive);
@@ -2997,6 +3005,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     }
     t_sync();
     EC_DBG(0, k);
+    EC_EPOCH_SYNC(W::NT); /* lockstep builds: co-resident teams start each epoch together */
     epoch_event<W, DCAP>(w, g, k);
     EC_DBG(1, k);
     /* watchdog: every batch commits or executes at least one event, so a

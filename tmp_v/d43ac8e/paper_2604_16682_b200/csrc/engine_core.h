@@ -83,16 +83,15 @@
   } while (0)
 #endif
 
-/* EC_LDK_* / EC_STK_*: loads / stores of the alive slots that every
+/* EC_LDK_* / EC_STK_*: loads / stores of the alive-slot arrays that every
  * epoch's sweep reads, marked to stay in L2 (evict_last) on the GPU */
-#ifndef EC_SLOT_ACCESSORS
+#ifndef EC_LDK_F64
+#define EC_LDK_F64(p) (*(p))
 #define EC_LDK_I32(p) (*(p))
+#define EC_LDK_F64X2(p, a, b) ((a) = (p)[0], (b) = (p)[1])
+#define EC_LDK_I32X2(p, a, b) ((a) = (p)[0], (b) = (p)[1])
 #define EC_STK_F64(p, v) (*(p) = (v))
 #define EC_STK_I32(p, v) (*(p) = (v))
-/* one 16-byte alive slot: (tp, nx, meta) */
-#define EC_LDK_SLOT(p, tp_, nx_, mt_) ((tp_) = (p)->tp, (nx_) = (p)->nx, (mt_) = (p)->meta)
-/* the slot's (nx, meta) half in one 8-byte store */
-#define EC_STK_EV(p, nx_, mt_) ((p)->nx = (nx_), (p)->meta = (mt_))
 #endif
 
 #ifndef EC_DEPCAP
@@ -125,25 +124,6 @@ struct Rec {
   int logpos;          /* start: position in the instance running log */
   int inst;
 };
-
-/* one alive slot, what every epoch's agent-tick sweep reads (16 bytes, one
- * vector load): the running throughput (+inf = None, NaN = finished), the
- * next event time rounded DOWN to f32 (a conservative due test: the exact
- * time is H[a].next_t, re-checked by the speculation, so a slot whose f32
- * time is in the window but whose exact time is not becomes an empty
- * candidate), and meta = instance | next-event kind << 7 | agent << 10, so
- * that collecting a due slot needs no second (dependent) load for its agent */
-struct alignas(16) Slot {
-  double tp;
-  float nx;
-  int meta;
-};
-static_assert(sizeof(Slot) == 16, "one 16-byte vector load per slot");
-#define EC_SLOT_MAX_AGENTS (1 << 21) /* agent ids in meta bits 10..30 (packing.py checks) */
-EC_DEV int slot_meta(int inst, int prio, int a) { return inst | (prio << 7) | (a << 10); }
-EC_DEV int sm_inst(int m) { return m & 0x7f; }
-EC_DEV int sm_prio(int m) { return (m >> 7) & 7; }
-EC_DEV int sm_agent(int m) { return m >> 10; }
 
 struct SortE {
   unsigned long long tb; /* time bits (times are >= 0, so bits order like values) */
@@ -202,7 +182,10 @@ struct GP {
   long long *o_dec, *o_maxctx, *o_ctx;
   int *o_steps, *o_inst, *o_mig, *o_phase;
   /* alive slots: the agent-tick / due sweeps read only these, coalesced */
-  Slot* sl;        /* (throughput, next event time, instance | kind | agent) per slot */
+  int* alive;      /* slot -> agent */
+  double* s_tp;    /* running throughput; +inf = None; NaN = finished */
+  double* s_next;  /* next event time */
+  int* s_meta;     /* instance | next-event kind << 8 */
   int* ring;       /* [M*A] pending FIFOs */
   int* log;        /* [M*A] running logs (insertion order of inst.running) */
   /* outputs */
@@ -411,21 +394,16 @@ EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long lon
   g.H[a].next_prio = prio;
   g.H[a].next_seq = seq;
   const int j = g.H[a].slot;
-  EC_STK_EV(&g.sl[j], ec_f32_down(t), slot_meta(inst, prio, a));
+  EC_STK_F64(&g.s_next[j], t);
+  EC_STK_I32(&g.s_meta[j], inst | (prio << 8));
 }
 
 EC_DEV void clear_event(const GP& g, int a, int inst) {
   g.H[a].next_prio = 0;
-  EC_STK_EV(&g.sl[g.H[a].slot], EC_INF_F32, slot_meta(inst, 0, a));
+  EC_STK_I32(&g.s_meta[g.H[a].slot], inst);
 }
 
-EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.sl[g.H[a].slot].tp, tp); }
-
-/* a fresh slot j for agent a: pending on instance `inst`, no throughput yet */
-EC_DEV void init_slot(const GP& g, int j, int inst, int a) {
-  EC_STK_F64(&g.sl[j].tp, EC_INF);
-  EC_STK_EV(&g.sl[j], 0.0f, slot_meta(inst, 0, a));
-}
+EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.s_tp[g.H[a].slot], tp); }
 
 template <class W>
 EC_COLD4 double svc_time(const W* w, const GP& g, long long turn, int level, int concurrent, int thr) {
@@ -566,8 +544,11 @@ EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos
   g.H[a].phase = ASB_PHASE_PENDING;
   g.H[a].next_prio = 0;
   const int j = w->n_alive++;
+  EC_STK_I32(&g.alive[j], a);
   g.H[a].slot = j;
-  init_slot(g, j, target, a);
+  EC_STK_F64(&g.s_tp[j], EC_INF);
+  EC_STK_F64(&g.s_next[j], 0.0);
+  EC_STK_I32(&g.s_meta[j], target);
   g.rank[a] = w->arr_rank++;
   w->arr_ptr = order_pos + 1;
   w->ctr[ASB_CTR_ARRIVED]++;
@@ -1034,7 +1015,7 @@ EC_DEV void fork_job(W* w, int job) {
   EC_LANE0 w->job = job;
   t_sync();
   ec_fork_begin(W::NT);
-  do_job(w, job, EC_TID_OF(W::NT), W::NT);
+  do_job(w, job, EC_TID, W::NT);
   ec_fork_end(W::NT);
 }
 
@@ -1044,7 +1025,7 @@ EC_DEV void helper_loop(W* w) {
     ec_fork_begin(W::NT);
     const int job = w->job;
     if (job == JOB_EXIT) break;
-    do_job(w, job, EC_TID_OF(W::NT), W::NT);
+    do_job(w, job, EC_TID, W::NT);
     ec_fork_end(W::NT);
   }
 }
@@ -1055,45 +1036,43 @@ EC_DEV void helper_loop(W* w) {
  * whose next event falls before j_bound become due candidates (stamped
  * j_token). */
 template <class W>
-EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
+EC_DEV void job_sweep_scalar(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
   const bool tick = w->j_tick, collect = w->j_collect != 0, count_only = w->j_collect == 2;
   const double bound = w->j_bound;
-  /* the slots hold next-event times rounded down to f32: comparing them
-   * with the bound is a conservative due test (see Slot) */
   const int incl = w->j_incl, token = w->j_token;
   const int n = w->n_alive;
   int dead = 0, counted = 0;
-#if defined(ASB_PROFILE_SWEEP)
-  const long long js_t0 = ec_clock();
-#endif
-  /* software-pipelined: the next chunk's 16-byte slot loads are in flight
-   * while this chunk is folded */
-  double tp[U], tp2[U];
-  float nx[U], nx2[U];
+  /* software-pipelined: the next chunk's loads are in flight while this
+   * chunk is folded */
+  double tp[U], nx[U], tp2[U], nx2[U];
   int mt[U], mt2[U];
 #pragma unroll
   for (int u = 0; u < U; u++) {
     const int j = u * nthr + tid;
-    mt[u] = -1;
-    if (j < n) EC_LDK_SLOT(&g.sl[j], tp[u], nx[u], mt[u]);
+    const bool ok = j < n;
+    mt[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
+    tp[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
+    nx[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
   }
   for (int base = 0; base < n; base += nthr * U) {
     const int nb = base + nthr * U;
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int j = nb + u * nthr + tid;
-      mt2[u] = -1;
-      if (j < n) EC_LDK_SLOT(&g.sl[j], tp2[u], nx2[u], mt2[u]);
+      const bool ok = j < n;
+      mt2[u] = ok ? EC_LDK_I32(&g.s_meta[j]) : -1;
+      tp2[u] = ok && tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0;
+      nx2[u] = ok && collect ? EC_LDK_F64(&g.s_next[j]) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (mt[u] < 0) continue;
-      if (collect && sm_prio(mt[u]) > 0 && (incl ? (double)nx[u] <= bound : (double)nx[u] < bound)) {
+      if (collect && (mt[u] >> 8) > 0 && (incl ? nx[u] <= bound : nx[u] < bound)) {
         if (count_only) {
           counted++;
         } else {
-          const int a = sm_agent(mt[u]);
+          const int a = EC_LDK_I32(&g.alive[base + u * nthr + tid]); /* only due slots need the agent id */
           const int pos = t_atomic_add_i(&w->j_total, 1);
           if (pos < W::DC) w->due[pos] = a;
           g.dstamp[a] = token;
@@ -1106,8 +1085,8 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       const unsigned long long b = ec_bits(tp[u]);
       if (b > EC_INF_BITS)
         dead++;
-      else if (b < w->tmin[sm_inst(mt[u]) - 1])
-        t_atomic_min_ull(&w->tmin[sm_inst(mt[u]) - 1], b);
+      else if (b < w->tmin[(mt[u] & 0xff) - 1])
+        t_atomic_min_ull(&w->tmin[(mt[u] & 0xff) - 1], b);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -1118,10 +1097,110 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   }
   if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
   if (counted) t_atomic_add_i(&w->j_total, counted);
-#if defined(ASB_PROFILE_SWEEP)
-  /* a helper's (thread 32's) time inside the tick sweeps: load rounds + fold */
-  if (tid == 32 && tick) w->prof[2] += ec_clock() - js_t0;
-#endif
+}
+
+template <class W>
+EC_DEV void job_sweep_pairs(W* w, const GP& g, int tid, int nthr) {
+  constexpr int U = EC_SWEEP_UNROLL;
+  const bool tick = w->j_tick, collect = w->j_collect != 0, count_only = w->j_collect == 2;
+  const double bound = w->j_bound;
+  const int incl = w->j_incl, token = w->j_token;
+  const int n = w->n_alive;
+  int dead = 0, counted = 0;
+  auto slot = [&](int j, int mt, double tp, double nx) {
+    if (collect && (mt >> 8) > 0 && (incl ? nx <= bound : nx < bound)) {
+      if (count_only) {
+        counted++;
+      } else {
+        const int a = EC_LDK_I32(&g.alive[j]); /* only due slots need the agent id */
+        const int pos = t_atomic_add_i(&w->j_total, 1);
+        if (pos < W::DC) w->due[pos] = a;
+        g.dstamp[a] = token;
+      }
+    }
+    if (!tick) return;
+    /* throughputs are >= 0, so the f64 bit patterns order like the values;
+     * +inf = None (no LLM time yet) never lowers the min; the positive
+     * quiet NaN marks a finished agent (not in process) */
+    const unsigned long long b = ec_bits(tp);
+    if (b > EC_INF_BITS)
+      dead++;
+    else if (b < w->tmin[(mt & 0xff) - 1])
+      t_atomic_min_ull(&w->tmin[(mt & 0xff) - 1], b);
+  };
+  /* slots go in pairs (off + 2q, off + 2q + 1) with 16-byte loads; the
+   * per-scenario arrays start on an odd slot when the scenario's first agent
+   * row is odd (off = 1), and that first slot and a last unpaired one go
+   * alone */
+  const int off = n > 0 ? (int)((reinterpret_cast<unsigned long long>(g.s_tp) >> 3) & 1) : 0;
+  const int np = (n - off) >> 1;
+  if (tid == 0 && off)
+    slot(0, EC_LDK_I32(&g.s_meta[0]), tick ? EC_LDK_F64(&g.s_tp[0]) : 0.0, collect ? EC_LDK_F64(&g.s_next[0]) : 0.0);
+  if (tid == nthr - 1 && n > off && ((n - off) & 1)) {
+    const int j = n - 1;
+    slot(j, EC_LDK_I32(&g.s_meta[j]), tick ? EC_LDK_F64(&g.s_tp[j]) : 0.0, collect ? EC_LDK_F64(&g.s_next[j]) : 0.0);
+  }
+  /* software-pipelined: the next chunk's loads are in flight while this
+   * chunk is folded */
+  double tpa[U], tpb[U], nxa[U], nxb[U], tpa2[U], tpb2[U], nxa2[U], nxb2[U];
+  int mta[U], mtb[U], mta2[U], mtb2[U];
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int q = u * nthr + tid;
+    const int j = off + 2 * q;
+    mta[u] = mtb[u] = -1;
+    tpa[u] = tpb[u] = nxa[u] = nxb[u] = 0.0;
+    if (q < np) {
+      EC_LDK_I32X2(&g.s_meta[j], mta[u], mtb[u]);
+      if (tick) EC_LDK_F64X2(&g.s_tp[j], tpa[u], tpb[u]);
+      if (collect) EC_LDK_F64X2(&g.s_next[j], nxa[u], nxb[u]);
+    }
+  }
+  for (int base = 0; base < np; base += nthr * U) {
+    const int nb = base + nthr * U;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int q = nb + u * nthr + tid;
+      const int j = off + 2 * q;
+      mta2[u] = mtb2[u] = -1;
+      tpa2[u] = tpb2[u] = nxa2[u] = nxb2[u] = 0.0;
+      if (q < np) {
+        EC_LDK_I32X2(&g.s_meta[j], mta2[u], mtb2[u]);
+        if (tick) EC_LDK_F64X2(&g.s_tp[j], tpa2[u], tpb2[u]);
+        if (collect) EC_LDK_F64X2(&g.s_next[j], nxa2[u], nxb2[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (mta[u] < 0) continue; /* past the last pair */
+      const int j = off + 2 * (base + u * nthr + tid);
+      slot(j, mta[u], tpa[u], nxa[u]);
+      slot(j + 1, mtb[u], tpb[u], nxb[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      mta[u] = mta2[u];
+      mtb[u] = mtb2[u];
+      tpa[u] = tpa2[u];
+      tpb[u] = tpb2[u];
+      nxa[u] = nxa2[u];
+      nxb[u] = nxb2[u];
+    }
+  }
+  if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
+  if (counted) t_atomic_add_i(&w->j_total, counted);
+}
+
+/* the 16-warp team sweeps tens of thousands of slots: pairs of slots per
+ * 16-byte load (C4: 578 -> 551 ms); the smaller teams keep the scalar
+ * sweep, whose smaller code suits 4-14 co-resident teams per SM (the
+ * paired sweep cost C5 +4% and C3 +6% through the instruction cache) */
+template <class W>
+EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
+  if (W::NT >= 512)
+    job_sweep_pairs(w, g, tid, nthr);
+  else
+    job_sweep_scalar(w, g, tid, nthr);
 }
 
 /* agent-tick sweep (main warp): fork the slot sweep, fold the partial
@@ -1159,19 +1238,22 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
       int j = base + EC_LANE;
       bool live = false;
       int a = -1, mt = 0;
-      double tp = 0.0;
-      float nx = 0.0f;
+      double tp = 0.0, nx = 0.0;
       if (j < n) {
-        EC_LDK_SLOT(&g.sl[j], tp, nx, mt);
+        tp = g.s_tp[j];
         live = !ec_isnan(tp);
-        a = sm_agent(mt);
+        a = g.alive[j];
+        nx = g.s_next[j];
+        mt = g.s_meta[j];
       }
       unsigned m = t_ballot(live);
       t_sync();
       if (live) {
         const int o = out + ec_popc(m & t_lt_mask());
-        EC_STK_F64(&g.sl[o].tp, tp);
-        EC_STK_EV(&g.sl[o], nx, mt);
+        EC_STK_I32(&g.alive[o], a);
+        EC_STK_F64(&g.s_tp[o], tp);
+        EC_STK_F64(&g.s_next[o], nx);
+        EC_STK_I32(&g.s_meta[o], mt);
         g.H[a].slot = o;
       }
       out += ec_popc(m);
@@ -1498,6 +1580,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   /* (d)+(e) re-time in-flight turns where the rate key changed, then start
    * the admitted turns — instances in parallel, one warp each (JOB_EPOCH) */
   if (nwork) {
+    EC_SPROF_CNT(w, 2);
     fork_job(w, JOB_EPOCH);
   }
   /* (f) lane per instance: final power, decision rows */
@@ -1828,7 +1911,7 @@ EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
     }
     w->snap[k][i - 1] = lo > w->ioff[i - 1] ? w->wu[lo - 1] : w->in[i - 1].usage;
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   const double threshold = sc.consolidation_threshold * (double)sc.capacity;
   for (int k = tid >> 5; k < n_dep; k += nthr >> 5) {
     const int p = w->dep_pos[k];
@@ -2160,8 +2243,11 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
         g.H[a].phase = ASB_PHASE_PENDING;
         g.H[a].next_prio = 0;
         const int j = w->n_alive + rank;
+        EC_STK_I32(&g.alive[j], a);
         g.H[a].slot = j;
-        init_slot(g, j, target, a);
+        EC_STK_F64(&g.s_tp[j], EC_INF);
+        EC_STK_F64(&g.s_next[j], 0.0);
+        EC_STK_I32(&g.s_meta[j], target);
         g.rank[a] = w->arr_rank + rank;
       }
       t_sync(); /* every lane has read fifo_len before the groups advance it */
@@ -2383,7 +2469,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
       const SKey k = skey_of(w, j, n_all); /* j >= n_all: (~0, ~0), sorts last */
       key[j] = make_ulonglong2(k.k1, k.k2);
     }
-    ec_team_barrier(W::NT);
+    ec_team_barrier();
     for (int k = 2; k <= N; k <<= 1) {
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
         for (int i = tid; i < N; i += nthr) {
@@ -2397,7 +2483,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
             }
           }
         }
-        ec_team_barrier(W::NT);
+        ec_team_barrier();
       }
     }
     for (int p = tid; p < n_all; p += nthr) {
@@ -2409,7 +2495,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     const SKey k = skey_of(w, j, n_all);
     key[j] = make_ulonglong2(k.k1, k.k2);
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   for (int j = tid; j < n_all; j += nthr) {
     const ulonglong2 me = key[j];
     int rank = 0;
@@ -2429,7 +2515,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     emit(j, rank, me.x);
   }
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   /* exact (time, prio) ties with an unknown push seq need the serial walk */
   int tie_unknown = 0;
   for (int p = tid + 1; p < n_all; p += nthr) {
@@ -2482,7 +2568,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     w->ks[j] = r.seq;
     w->ki[j] = (short)(empty || r.prio == EV_ARRIVAL ? 0 : r.inst);
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   int tie_unknown = 0;
   for (int j = tid; j < n_all; j += nthr) {
     if (w->kp[j] == 0xff) continue;
@@ -2525,7 +2611,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (!below_horizon(tj, pj, sj, w->hz_t, (unsigned)w->hz_p, w->hz_s)) t_atomic_min_i(&w->j_cut, rank);
   }
   if (tie_unknown) w->j_tie_unknown = 1;
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   if (tid < EC_TSIZE) { /* warp 0: exclusive scan of the per-instance record counts */
     long long run = 0;
     for (int base = 0; base < M; base += EC_TSIZE) {
@@ -2537,7 +2623,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     }
     EC_LANE0 w->ioff[M] = (int)run;
   }
-  ec_team_barrier(W::NT);
+  ec_team_barrier();
   for (int j = tid; j < n_all; j += nthr) {
     const int ij = w->ki[j];
     if (ij && w->kp[j] != 0xff) w->ilist[w->ioff[ij - 1] + w->kir[j]] = w->krank[j];
@@ -2879,8 +2965,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
 }
 
 /* exact single-event fallback: process the minimum pending event serially
- * (the timeseries loop, and a burst of identical timestamps larger than the
- * batch buffers) */
+ * (used only when a burst of identical timestamps exceeds the batch buffers) */
 template <class W>
 EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   EC_DBG(11, w->n_alive);
@@ -2889,11 +2974,10 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   long long bs = 0x7fffffffffffffffll;
   int ba = -1;
   for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
-    const int mt = g.sl[j].meta;
-    const int pr = sm_prio(mt);
+    const int pr = g.s_meta[j] >> 8;
     if (pr <= 0) continue;
-    const int a = sm_agent(mt);
-    unsigned long long tb = ec_bits(g.H[a].next_t); /* the exact time (the slot's is rounded down) */
+    const int a = g.alive[j];
+    unsigned long long tb = ec_bits(g.s_next[j]);
     long long s = g.H[a].next_seq;
     if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
       bt = tb;

@@ -77,6 +77,15 @@
 
 /* EC_DBG(slot, value): progress markers for hang debugging (GPU debug build
  * -DASB_DEBUG_TRACE writes them to host-mapped memory); no-op otherwise */
+/* EC_EPOCH_SYNC(nt): an includer hook run by the main warp at the start of
+ * every control epoch (the GPU lockstep kernels align the teams sharing a
+ * CTA there); no-op by default */
+#ifndef EC_EPOCH_SYNC
+#define EC_EPOCH_SYNC(nt) \
+  do {                    \
+  } while (0)
+#endif
+
 #ifndef EC_DBG
 #define EC_DBG(slot, value) \
   do {                      \
@@ -2878,21 +2887,30 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   return BATCH_DONE;
 }
 
-/* exact single-event fallback: process the minimum pending event serially
- * (the timeseries loop, and a burst of identical timestamps larger than the
- * batch buffers) */
+/* exact single-event step: process the minimum pending event serially.
+ * `cand`: the minimum over the window's due candidates (w->due, kept
+ * complete by cand_collect) — the small-window path; otherwise over every
+ * alive slot — the timeseries loop and the fallback for a burst of
+ * identical timestamps larger than the batch buffers. */
 template <class W>
-EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
+EC_COLD2 bool serial_step(W* w, const GP& g, double win_end, bool cand = false) {
   EC_DBG(11, w->n_alive);
   unsigned long long bt = EC_INF_BITS;
   unsigned bp = 0xffffffffu;
   long long bs = 0x7fffffffffffffffll;
   int ba = -1;
-  for (int j = EC_LANE; j < w->n_alive; j += EC_TSIZE) {
-    const int mt = g.sl[j].meta;
-    const int pr = sm_prio(mt);
+  const int n = cand ? w->n_cand : w->n_alive;
+  for (int j = EC_LANE; j < n; j += EC_TSIZE) {
+    int a, pr;
+    if (cand) {
+      a = w->due[j];
+      pr = g.H[a].next_prio;
+    } else {
+      const int mt = g.sl[j].meta;
+      pr = sm_prio(mt);
+      a = sm_agent(mt);
+    }
     if (pr <= 0) continue;
-    const int a = sm_agent(mt);
     unsigned long long tb = ec_bits(g.H[a].next_t); /* the exact time (the slot's is rounded down) */
     long long s = g.H[a].next_seq;
     if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
@@ -2948,6 +2966,48 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   return true;
 }
 
+/* Small windows (C3: a couple of events per epoch) skip the optimistic
+ * batch: when the epoch's due candidates plus the window's arrivals number
+ * at most EC_SERIAL_MAX, the window's events run one at a time in the exact
+ * (time, priority, seq) order, each the minimum over the candidate list —
+ * the speculate / sort / walk / apply machinery costs far more than a few
+ * serial handlers.  Re-timed turns join the candidates as they happen
+ * (cand_collect, as for a batch's coupling follow-up).  Returns false when
+ * the window does not qualify or the candidate list overflows; the batch
+ * loop then finishes the window from wherever the serial steps stopped. */
+#ifndef EC_SERIAL_MAX
+#define EC_SERIAL_MAX 6
+#endif
+template <class W>
+EC_COLD3 bool serial_window(W* w, const GP& g, double win_end) {
+  if (!w->due_ready || w->n_cand > EC_SERIAL_MAX) return false;
+  /* arrivals in the window: a prefix of the sorted arrival times */
+  {
+    const int p = w->arr_ptr + EC_LANE;
+    const double t = p < g.A ? g.arr_t[p] : EC_INF;
+    const bool in = p < g.A && t < w->sc.sim_duration && (w->incl ? t <= win_end : t < win_end);
+    if (w->n_cand + ec_popc(t_ballot(in)) > EC_SERIAL_MAX) return false;
+  }
+  EC_LANE0 {
+    w->due_ready = 0;
+    w->cand_collect = 1; /* candidates keep the tick sweep's token (w->cand_token) */
+    w->ctr[ASB_CTR_BATCHES]++;
+  }
+  t_sync();
+  bool done = true;
+  for (;;) {
+    if (w->status) break;
+    if (w->n_cand > W::DC) { /* re-timing overflowed the list: the batch loop recollects */
+      done = false;
+      break;
+    }
+    if (!serial_step(w, g, win_end, true)) break;
+  }
+  EC_LANE0 w->cand_collect = 0;
+  t_sync();
+  return done;
+}
+
 /* TS: the scenario writes timeseries rows (g.ts_rows) and runs the exact
  * serial loop; a separate instantiation keeps the batched engine's code
  * unchanged */
@@ -2997,12 +3057,14 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     }
     t_sync();
     EC_DBG(0, k);
+    EC_EPOCH_SYNC(W::NT); /* lockstep builds: co-resident teams start each epoch together */
     epoch_event<W, DCAP>(w, g, k);
     EC_DBG(1, k);
     /* watchdog: every batch commits or executes at least one event, so a
      * window never needs more batches than live events + arrivals (+ the
      * window-shrink restarts); exceeding a generous bound is a bug */
     long long guard = 64 + 4 * (long long)(g.A + w->n_alive) + 8 * (long long)g.A;
+    if (!TS && serial_window(w, g, win_end)) continue;
     for (;;) {
       if (w->status) break;
       if (--guard < 0) {

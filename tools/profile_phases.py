@@ -12,7 +12,8 @@ from paper_2604_16682_b200 import _build  # noqa: E402
 
 WALK = os.environ.get("ASB_PROFILE_WALK") == "1"
 SWEEP = os.environ.get("ASB_PROFILE_SWEEP") == "1"
-os.environ["ASB_LIB"] = _build.build_cuda(profile="walk" if WALK else ("sweep" if SWEEP else True))
+os.environ["ASB_LIB"] = os.environ.get("ASB_PROF_LIB") or _build.build_cuda(
+    profile="walk" if WALK else ("sweep" if SWEEP else True))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
