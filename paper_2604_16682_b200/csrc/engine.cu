@@ -87,10 +87,6 @@ EC_DEV int t_shfl_xor_i(int v, int o) { return __shfl_xor_sync(FULLMASK, v, o); 
 EC_DEV long long t_shfl_up_ll(long long v, int o) { return __shfl_up_sync(FULLMASK, v, o); }
 EC_DEV int t_shfl_up_i(int v, int o) { return __shfl_up_sync(FULLMASK, v, o); }
 EC_DEV void t_atomic_min_ull(unsigned long long* p, unsigned long long v) { atomicMin(p, v); }
-EC_DEV void t_atomic_min_u32(unsigned* p, unsigned v) { atomicMin(p, v); }
-EC_DEV unsigned ec_f32_bits(float f) { return (unsigned)__float_as_int(f); }
-EC_DEV float ec_f32_from_bits(unsigned b) { return __int_as_float((int)b); }
-#define EC_INF_F32_BITS 0x7f800000u
 EC_DEV int t_atomic_add_i(int* p, int v) { return atomicAdd(p, v); }
 EC_DEV bool ec_isnan(double x) { return isnan(x); }
 EC_DEV double ec_floor(double x) { return floor(x); }

@@ -271,8 +271,7 @@ struct WS {
   int stamp_ctr; /* last due-list stamp handed out (dstamp de-duplication) */
   double pr[16], dr[16], act[16], idle[16];
   Inst in[MAXM];
-  unsigned long long tmin[MAXM]; /* min running throughput (f64 bits) per instance */
-  unsigned fmin[MAXM];           /* the same min rounded down to f32 (bits): the sweep's native 32-bit atomics */
+  unsigned long long tmin[MAXM];
   /* epoch scratch (per instance) */
   long long ep_uobs[MAXM], ep_seq[MAXM];
   double ep_mintp[MAXM];
@@ -1058,11 +1057,7 @@ EC_DEV void helper_loop(W* w) {
 template <class W>
 EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   constexpr int U = EC_SWEEP_UNROLL;
-  /* j_tick 1: the agent-tick pass (f32 keys of the throughputs into fmin,
-   * dead-slot count, due collection); 2: the exact pass (64-bit minimum over
-   * the slots whose key ties their instance's fmin) */
-  const int tick_mode = w->j_tick;
-  const bool tick = tick_mode != 0, collect = w->j_collect != 0, count_only = w->j_collect == 2;
+  const bool tick = w->j_tick, collect = w->j_collect != 0, count_only = w->j_collect == 2;
   const double bound = w->j_bound;
   /* the slots hold next-event times rounded down to f32: comparing them
    * with the bound is a conservative due test (see Slot) */
@@ -1109,18 +1104,10 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
        * +inf = None (no LLM time yet) never lowers the min; the positive
        * quiet NaN marks a finished agent (not in process) */
       const unsigned long long b = ec_bits(tp[u]);
-      if (b > EC_INF_BITS) {
+      if (b > EC_INF_BITS)
         dead++;
-      } else {
-        /* f32 round-down is monotone, so the f32 minimum is the round-down
-         * of the f64 minimum and only slots tying it can hold the latter */
-        const int i = sm_inst(mt[u]) - 1;
-        const unsigned key = ec_f32_bits(ec_f32_down(tp[u]));
-        if (tick_mode == 1)
-          t_atomic_min_u32(&w->fmin[i], key); /* native, result unused: no stall */
-        else if (key == w->fmin[i] && b < w->tmin[i])
-          t_atomic_min_ull(&w->tmin[i], b);
-      }
+      else if (b < w->tmin[sm_inst(mt[u]) - 1])
+        t_atomic_min_ull(&w->tmin[sm_inst(mt[u]) - 1], b);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -1129,7 +1116,7 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       nx[u] = nx2[u];
     }
   }
-  if (tick_mode == 1 && dead) t_atomic_add_i(&w->j_dead, dead);
+  if (tick && dead) t_atomic_add_i(&w->j_dead, dead);
   if (counted) t_atomic_add_i(&w->j_total, counted);
 #if defined(ASB_PROFILE_SWEEP)
   /* a helper's (thread 32's) time inside the tick sweeps: load rounds + fold */
@@ -1155,39 +1142,10 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
     w->j_dead = 0;
     w->j_total = 0;
   }
-  for (int i = EC_LANE; i < M; i += EC_TSIZE) {
-    w->tmin[i] = EC_INF_BITS;
-    w->fmin[i] = EC_INF_F32_BITS; /* the sweep's 32-bit atomics fold into it */
-  }
+  for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS; /* the sweep's smem atomics fold into it */
   EC_SPROF_T0(w);
   fork_job(w, JOB_SWEEP);
   EC_SPROF_ADD(w, 0);
-  /* The f64 minimum m of instance i lies in [F, next f32 after F), F the
-   * f32 minimum.  The boost test m < tau (controller.py:106-109, 150-153)
-   * is decided by F unless tau falls strictly inside that interval; the
-   * exact m is needed then and for the decision rows.  Otherwise tmin holds
-   * F itself, which makes every decision the exact m would. */
-  {
-    const AsbScenario& sc = w->sc;
-    const bool boost = sc.variant == ASB_VARIANT_CONTEXT_AWARE && sc.boost_enabled;
-    bool exact = g.dec_rows != nullptr;
-    for (int i = EC_LANE; i < M; i += EC_TSIZE) {
-      const unsigned F = w->fmin[i];
-      if (F != EC_INF_F32_BITS) {
-        const double lo = (double)ec_f32_from_bits(F), hi = (double)ec_f32_from_bits(F + 1);
-        if (boost && lo < sc.slo_target && sc.slo_target < hi) exact = true;
-        w->tmin[i] = ec_bits(lo);
-      }
-    }
-    if (t_ballot(exact)) {
-      for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS;
-      EC_LANE0 {
-        w->j_tick = 2;
-        w->j_collect = 0;
-      }
-      fork_job(w, JOB_SWEEP);
-    }
-  }
   const int dead_all = w->j_dead;
   EC_LANE0 {
     w->ctr[ASB_CTR_TICKS] += n - dead_all;

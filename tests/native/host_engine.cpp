@@ -36,10 +36,6 @@ static inline int t_shfl_xor_i(int v, int) { return v; }
 static inline long long t_shfl_up_ll(long long v, int) { return v; }
 static inline int t_shfl_up_i(int v, int) { return v; }
 static inline void t_atomic_min_ull(unsigned long long* p, unsigned long long v) { if (v < *p) *p = v; }
-static inline void t_atomic_min_u32(unsigned* p, unsigned v) { if (v < *p) *p = v; }
-static inline unsigned ec_f32_bits(float f) { unsigned b; memcpy(&b, &f, 4); return b; }
-static inline float ec_f32_from_bits(unsigned b) { float f; memcpy(&f, &b, 4); return f; }
-#define EC_INF_F32_BITS 0x7f800000u
 static inline int t_atomic_add_i(int* p, int v) { int o = *p; *p += v; return o; }
 static inline bool ec_isnan(double x) { return x != x; }
 static inline double ec_floor(double x) { return floor(x); }

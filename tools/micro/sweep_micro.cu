@@ -69,11 +69,6 @@ __global__ void __launch_bounds__(128, 4) sweep(const Slot* sl, int n, int reps,
         else if (MODE == 4) { /* per-warp private copies */
           unsigned long long* tw = wmin[threadIdx.x >> 5];
           if (b < tw[i]) atomicMin(&tw[i], b);
-        } else if (MODE == 8) { /* fire-and-forget 32-bit min of the f32 round-down key (native ATOMS.MIN) */
-          atomicMin(&fmin[i], (unsigned)__float_as_int(__double2float_rd(tp[u])));
-        } else if (MODE == 9) { /* guarded 32-bit key min */
-          const unsigned f = (unsigned)__float_as_int(__double2float_rd(tp[u]));
-          if (f < fmin[i]) atomicMin(&fmin[i], f);
         } else if (MODE == 6) { /* fire-and-forget 64-bit min in L2 */
           asm volatile("red.relaxed.gpu.global.min.u64 [%0], %1;" ::"l"(gt + i), "l"(b) : "memory");
         } else if (MODE == 5) { /* f32 round-down key: native 32-bit min, 64-bit CAS only for candidates */
@@ -155,7 +150,6 @@ int main() {
   };
   run("U=2 atomic", sweep<2, 0>); run("U=2 racy", sweep<2, 1>); run("U=2 no-min", sweep<2, 2>);
 run("U=2 per-warp copies", sweep<2, 4>); run("U=2 f32 key", sweep<2, 5>);
-  run("U=2 f32 ff atomic", sweep<2, 8>); run("U=2 f32 guarded", sweep<2, 9>); run("U=4 f32 ff atomic", sweep<4, 8>);
   run("U=2 batched guards", sweep<2, 7>); run("U=4 batched guards", sweep<4, 7>); run("U=8 batched guards", sweep<8, 7>); run("U=4 no-min", sweep<4, 2>);
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
