@@ -383,6 +383,10 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem) != cudaSuccess || per_sm < 1)
     return ASB_ERR_LAUNCH;
+  if (const char* cap_env = getenv("ASB_TEAMS_PER_SM")) { /* experiment: fewer co-resident teams */
+    const int c = atoi(cap_env);
+    if (c >= 1 && c < per_sm) per_sm = c;
+  }
   if (getenv("ASB_DEBUG_LAUNCH"))
     fprintf(stderr, "asb launch: team %d, smem %zu B, %d blocks/SM, %d SMs\n", NT, smem, per_sm, sms);
   long long want = n_scen;

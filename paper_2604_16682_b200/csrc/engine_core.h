@@ -1859,6 +1859,12 @@ EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
 #ifndef EC_WIDE_LANE_PAR
 #define EC_WIDE_LANE_PAR 1
 #endif
+/* multi-warp teams with <= 32 instances: snapshots, checks and arrival
+ * routing as the same team job (a warp per dependent record) instead of one
+ * warp reduction per record in order on the main warp */
+#ifndef EC_TEAM_DEPS_SMALL
+#define EC_TEAM_DEPS_SMALL 1
+#endif
 
 /* Parallel commit walk (team).  The serial walk's state machine decomposes
  * by instance: usage, running count, thrash flag, power and the running log
@@ -1976,7 +1982,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
    * one binary search per (record, instance) pair across the lanes; many
    * instances (M > 32): lane per instance, merging its sorted record list
    * with the sorted dependent positions */
-  const bool team_deps = W::NW > 1 && W::MX > 32 && M > EC_TSIZE && n_dep > 0;
+  const bool team_deps = W::NW > 1 && n_dep > 0 && (M > EC_TSIZE ? W::MX > 32 : EC_TEAM_DEPS_SMALL);
   if (team_deps) {
     /* many instances, helper warps: snapshots, checks and routing as a team job */
     EC_LANE0 w->j_stop = stop_p;
@@ -2690,7 +2696,7 @@ EC_DEV void do_job(W* w, int job, int tid, int nthr) {
     case JOB_EPOCH: job_epoch(w, g, tid, nthr); break;
     case JOB_FINISH: job_finish(w, g, tid, nthr); break;
     case JOB_DEPS:
-      if (W::MX > 32) job_deps(w, g, tid, nthr);
+      if (W::NW > 1 && (W::MX > 32 || EC_TEAM_DEPS_SMALL)) job_deps(w, g, tid, nthr);
       break;
     default: break;
   }
@@ -2981,7 +2987,8 @@ EC_DEV void run_scenario(W* w, const GP& g) {
       w->ts_k = 1;
       for (int i = 0; i < M; i++) w->ts_last[i] = -1;
       /* run(), engine.py:576-579: a forced row per instance before any event */
-      for (int i = 1; i <= M; i++) mark_row(w, g, i, 0.0, true);
+      if (g.ts_rows)
+        for (int i = 1; i <= M; i++) mark_row(w, g, i, 0.0, true);
     }
   }
   t_sync();
@@ -3023,7 +3030,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
          * executes an event, so the watchdog does not apply) */
         guard++;
         if (!serial_step(w, g, win_end)) {
-          EC_LANE0 ts_samples(w, g, win_end);
+          EC_LANE0 if (g.ts_rows) ts_samples(w, g, win_end);
           t_sync();
           break;
         }
@@ -3055,7 +3062,8 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     t_sync();
     EC_LANE0 {
       /* engine.py:595-603: a forced row per instance at the end */
-      for (int i = 1; i <= M; i++) mark_row(w, g, i, T, true);
+      if (g.ts_rows)
+        for (int i = 1; i <= M; i++) mark_row(w, g, i, T, true);
       if (g.ts_count) *g.ts_count = w->ts_n;
     }
     t_sync();
