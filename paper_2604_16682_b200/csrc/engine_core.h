@@ -98,8 +98,16 @@
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
+/* loops over instances: kept rolled, the trip count is small and the
+ * co-resident teams share a 32 KB instruction cache */
+#ifndef EC_ILOOP
+#define EC_ILOOP _Pragma("unroll 1")
+#endif
 #ifndef EC_SWEEP_UNROLL
 #define EC_SWEEP_UNROLL 2 /* independent loads in flight per lane in the slot sweeps (small: I-cache) */
+#endif
+#ifndef EC_SWEEP_UNROLL_QUAD
+#define EC_SWEEP_UNROLL_QUAD EC_SWEEP_UNROLL /* the same for the 4-warp team */
 #endif
 
 namespace asb {
@@ -898,7 +906,7 @@ EC_DEV void cur_turn_pd(const GP& g, const Cur& c, int& p, int& d) {
 
 /* service_time (instance.py:184-204) from the token counts */
 template <class W>
-EC_DEV double svc_time_pd(const W* w, int p, int d, int level, int concurrent, int thr) {
+EC_COLD4 double svc_time_pd(const W* w, int p, int d, int level, int concurrent, int thr) {
   double base = (double)p / w->pr[level - 1] + (double)d / w->dr[level - 1];
   int extra = concurrent - 1 > 0 ? concurrent - 1 : 0;
   double factor = 1.0 + w->sc.interference * (double)extra;
@@ -1056,7 +1064,7 @@ EC_DEV void helper_loop(W* w) {
  * j_token). */
 template <class W>
 EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
-  constexpr int U = EC_SWEEP_UNROLL;
+  constexpr int U = W::NT == 128 ? EC_SWEEP_UNROLL_QUAD : EC_SWEEP_UNROLL;
   const bool tick = w->j_tick, collect = w->j_collect != 0, count_only = w->j_collect == 2;
   const double bound = w->j_bound;
   /* the slots hold next-event times rounded down to f32: comparing them
@@ -1106,8 +1114,14 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       const unsigned long long b = ec_bits(tp[u]);
       if (b > EC_INF_BITS)
         dead++;
+#if defined(ASB_EXP_SWEEP_NOMIN)
+      else if (b == 1) w->tmin[0] = b; /* experiment: no min */
+#elif defined(ASB_EXP_SWEEP_RACY)
+      else if (b < w->tmin[sm_inst(mt[u]) - 1]) w->tmin[sm_inst(mt[u]) - 1] = b; /* experiment: racy */
+#else
       else if (b < w->tmin[sm_inst(mt[u]) - 1])
         t_atomic_min_ull(&w->tmin[sm_inst(mt[u]) - 1], b);
+#endif
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -1142,6 +1156,7 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
     w->j_dead = 0;
     w->j_total = 0;
   }
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE; i < M; i += EC_TSIZE) w->tmin[i] = EC_INF_BITS; /* the sweep's smem atomics fold into it */
   EC_SPROF_T0(w);
   fork_job(w, JOB_SWEEP);
@@ -1398,6 +1413,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   }
   const double now = w->now;
   /* (a) lane per instance: observe, level, boost, level-hook power */
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     Inst& in = w->in[i - 1];
     int boosted;
@@ -1416,6 +1432,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   const double bcap = (ca ? sc.beta : 1.0) * (double)sc.capacity;
   {
     int cnt = 0;
+    EC_ILOOP /* per-instance loop: rolled (instruction cache) */
     for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
       const int i = r0 + EC_LANE + 1;
       /* pending agents and room below gamma * cap (else admission_pass admits nothing) */
@@ -1443,6 +1460,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   int flips = 0;
   long long extra_retimes = 0, all_retimes = 0;
   int nwork = 0;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
     const int i = r0 + EC_LANE + 1;
     long long pushes = 0, starts = 0;
@@ -1501,6 +1519,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
     fork_job(w, JOB_EPOCH);
   }
   /* (f) lane per instance: final power, decision rows */
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     update_power(w, i, now);
     write_decision(w, g, k, i);
@@ -1649,6 +1668,7 @@ EC_COLD2 void walk_serial(W* w, const GP& g, const int n) {
 template <class W>
 EC_COLD4 void snapshots_merge(W* w, int n_dep, int stop_p) {
   const int M = w->sc.n_instances;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     const int e1 = w->ioff[i];
     int e = w->ioff[i - 1];
@@ -1744,6 +1764,7 @@ EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* b
   const int M = w->sc.n_instances;
   unsigned key = 0xffffffffu;
   bool wide = false;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     const long long u = w->snap[k][i - 1];
     if (!(all || u > 0 || i == cur)) continue;
@@ -1784,6 +1805,7 @@ EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_
   }
   long long bu = 0;
   int bi = 0;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     const long long u = w->snap[k][i - 1];
     if (!all && !(u > 0 || i == cur)) continue;
@@ -1792,6 +1814,7 @@ EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_
       bi = i;
     }
   }
+  EC_ILOOP
   for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
     const long long ou = t_shfl_xor_ll(bu, o);
     const int oi = t_shfl_xor_i(bi, o);
@@ -1843,6 +1866,7 @@ EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
     } else if (pr == EV_ARRIVAL && sc.policy != ASB_POLICY_ROUND_ROBIN) {
       int light = 0;
       if (sc.policy == ASB_POLICY_CONTEXT_AWARE)
+        EC_ILOOP /* per-instance loop: rolled (instruction cache) */
         for (int base = 0; base < M && !light; base += 32) {
           const int i = base + EC_LANE + 1;
           const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
@@ -1899,6 +1923,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     }
     ndep += ec_popc(m);
   }
+  EC_ILOOP
   for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
     int oc = t_shfl_xor_i(cut, o);
     cut = oc < cut ? oc : cut;
@@ -1926,6 +1951,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     const bool comp = pr == EV_COMPLETE, start = pr == EV_TOOL || pr == EV_ISSUE;
     long long vu = comp ? w->sw_du[p] : 0;
     int vr = comp ? -1 : (start ? 1 : 0), vl = start ? 1 : 0;
+    EC_ILOOP
     for (int o = 1; o < EC_TSIZE; o <<= 1) {
       const long long nu = t_shfl_up_ll(vu, o);
       const int nr = t_shfl_up_i(vr, o), nl = t_shfl_up_i(vl, o);
@@ -2059,6 +2085,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     r.logpos = w->wl[e] - 1;
     g.log[(long long)(i - 1) * g.A + r.logpos] = r.agent;
   }
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     Inst& in = w->in[i - 1];
     const int e0 = w->ioff[i - 1];
@@ -2215,6 +2242,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
         int light = 0;
         if (sc.policy == ASB_POLICY_CONTEXT_AWARE) {
           const double threshold = sc.consolidation_threshold * (double)sc.capacity;
+          EC_ILOOP /* per-instance loop: rolled (instruction cache) */
           for (int base = 0; base < M && !light; base += EC_TSIZE) {
             const int i = base + EC_LANE + 1;
             const unsigned m = t_ballot(i <= M && (double)w->snap[k][i - 1] < threshold);
@@ -2368,6 +2396,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int M = w->sc.n_instances;
   const int lane = tid & 31, wid = tid >> 5;
   ulonglong2* key = reinterpret_cast<ulonglong2*>(w->skey);
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
   auto emit = [&](int j, int rank, unsigned long long tj) {
     const Rec& rr = w->rec[j];
@@ -2458,6 +2487,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
       __syncwarp();
     }
     long long run = 0;
+    EC_ILOOP /* per-instance loop: rolled (instruction cache) */
     for (int base = 0; base < M; base += 32) {
       const int i = base + lane;
       const long long c = i < M ? w->icnt[i] : 0;
@@ -2479,6 +2509,7 @@ template <class W>
 EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
   const int M = w->sc.n_instances;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
   for (int j = tid; j < n_all; j += nthr) {
     const Rec& r = w->rec[j];
@@ -2534,6 +2565,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   ec_team_barrier(W::NT);
   if (tid < EC_TSIZE) { /* warp 0: exclusive scan of the per-instance record counts */
     long long run = 0;
+    EC_ILOOP /* per-instance loop: rolled (instruction cache) */
     for (int base = 0; base < M; base += EC_TSIZE) {
       const int i = base + EC_LANE;
       const long long c = i < M ? w->icnt[i] : 0;
@@ -2963,6 +2995,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
   const int M = sc.n_instances, L = sc.n_levels;
   /* ---- init (engine.py:251-276) */
   fork_job(w, JOB_INIT);
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE; i < M; i += EC_TSIZE) {
     Inst& in = w->in[i];
     in.usage = 0;
@@ -3044,6 +3077,7 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     }
   }
   /* ---- final accounting (engine.py:595-603) and outputs */
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE; i < M; i += EC_TSIZE) {
     Inst& in = w->in[i];
     in.energy += in.watts * (T - in.t_pow);
