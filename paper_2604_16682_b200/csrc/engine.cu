@@ -453,6 +453,9 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
     solo = !strcmp(force, "solo");
   }
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+  /* single-instance scenarios (the DVFS sweep): a kernel whose instance
+   * count is the constant 1, with the per-instance machinery folded away */
+  if (max_instances == 1 && solo) return launch_engine<1, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16) {
     if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);

@@ -314,6 +314,14 @@ struct WS {
   long long ts_last[MAXM];
 };
 
+/* the scenario's instance count; a compile-time 1 in the single-instance
+ * kernels (MAXM = 1), so that their per-instance loops, scans and argmins
+ * fold away */
+template <class W>
+EC_DEV int ec_nm(const W* w) {
+  return W::MX == 1 ? 1 : w->sc.n_instances;
+}
+
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
  * accumulated by lane 0 and reported in counters[10..15];
  * -DASB_PROFILE -DASB_PROFILE_WALK times the commit-walk steps instead */
@@ -515,7 +523,7 @@ EC_COLD4 void ts_samples(W* w, const GP& g, double limit) {
   for (;;) {
     const double st = (double)w->ts_k * iv;
     if (!(st < limit && st < T) || w->status) break;
-    for (int i = 1; i <= w->sc.n_instances; i++) mark_row(w, g, i, st, true);
+    for (int i = 1; i <= ec_nm(w); i++) mark_row(w, g, i, st, true);
     w->ts_k++;
   }
 }
@@ -526,7 +534,7 @@ template <class W>
 EC_COLD4 int argmin_usage(const W* w, int cand_mode, int current) {
   int best = 0;
   long long bu = 0;
-  for (int i = 1; i <= w->sc.n_instances; i++) {
+  for (int i = 1; i <= ec_nm(w); i++) {
     long long u = w->in[i - 1].usage;
     if (cand_mode == 1 && !(u > 0 || i == current)) continue;
     if (!best || u < bu) {
@@ -552,13 +560,13 @@ template <class W>
 EC_COLD4 int route_arrival(W* w) {
   const AsbScenario& sc = w->sc;
   if (sc.policy == ASB_POLICY_ROUND_ROBIN) {
-    int t = (w->rr_next % sc.n_instances) + 1;
+    int t = (w->rr_next % ec_nm(w)) + 1;
     w->rr_next++;
     return t;
   }
   if (sc.policy == ASB_POLICY_LEAST_LOADED) return argmin_usage(w, 0, 0);
   double threshold = sc.consolidation_threshold * (double)sc.capacity;
-  for (int i = 1; i <= sc.n_instances; i++)
+  for (int i = 1; i <= ec_nm(w); i++)
     if ((double)w->in[i - 1].usage < threshold) return i;
   return argmin_usage(w, 0, 0);
 }
@@ -1143,7 +1151,7 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
  * ticks, and compact finished agents out lazily. */
 template <class W>
 EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl, int) {
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   const int n = w->n_alive;
   const int token = w->stamp_ctr + 1; /* a fresh stamp per due list */
   EC_LANE0 {
@@ -1323,7 +1331,7 @@ template <class W>
 EC_COLD4 void write_decision(W* w, const GP& g, long long k, int i) {
   if (!g.dec_rows) return;
   const Inst& in = w->in[i - 1];
-  AsbDecision& d = g.dec_rows[k * w->sc.n_instances + (i - 1)];
+  AsbDecision& d = g.dec_rows[k * ec_nm(w) + (i - 1)];
   d.time = w->now;
   d.min_throughput = w->tmin[i - 1] != EC_INF_BITS ? ec_from_bits(w->tmin[i - 1]) : EC_NAN;
   d.usage_observed = w->ep_uobs[i - 1];
@@ -1340,7 +1348,7 @@ template <class W>
 EC_COLD2 void epoch_serial(W* w, const GP& g, long long k) {
   EC_DBG(8, k);
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances;
+  const int M = ec_nm(w);
   for (int i = 1; i <= M; i++) {
     Inst& in = w->in[i - 1];
     EC_LANE0 {
@@ -1399,7 +1407,7 @@ EC_COLD2 void epoch_serial(W* w, const GP& g, long long k) {
 template <class W, int DCAP>
 EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances;
+  const int M = ec_nm(w);
   const bool collect = sc.interference == 0 && !g.ts_rows;
   EC_PROF_START(w);
   tick_sweep(w, g, collect, w->bound, w->incl, 0);
@@ -1667,7 +1675,7 @@ EC_COLD2 void walk_serial(W* w, const GP& g, const int n) {
  * merging its sorted record list with the sorted dependent positions */
 template <class W>
 EC_COLD4 void snapshots_merge(W* w, int n_dep, int stop_p) {
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     const int e1 = w->ioff[i];
@@ -1689,7 +1697,7 @@ EC_COLD4 void snapshots_merge(W* w, int n_dep, int stop_p) {
  * cand_mode 0 = all instances, 1 = reassignment candidates; 0 = none */
 template <class W>
 EC_DEV int snap_argmin_lane(const W* w, int k, bool all, int cur, long long* bu_out) {
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   long long bu = 0;
   int bi = 0;
   for (int i = 1; i <= M; i++) {
@@ -1730,7 +1738,7 @@ EC_COLD4 int checks_parallel(const W* w, int n_dep, int stop_p) {
 template <class W>
 EC_COLD4 void route_parallel(W* w, int n_dep, int stop_p) {
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances;
+  const int M = ec_nm(w);
   const double threshold = sc.consolidation_threshold * (double)sc.capacity;
   int before = 0; /* arrivals ahead of this lane's chunk */
   for (int base = 0; base < n_dep; base += EC_TSIZE) {
@@ -1761,7 +1769,7 @@ EC_COLD4 void route_parallel(W* w, int n_dep, int stop_p) {
  * key, one warp reduction; -1 when a usage does not fit the key */
 template <class W>
 EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* bu_out) {
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   unsigned key = 0xffffffffu;
   bool wide = false;
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
@@ -1786,7 +1794,7 @@ EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* b
  * (usage << 6 | id) key when every instance has a lane and usages fit. */
 template <class W>
 EC_DEV int snap_argmin(const W* w, int k, int cand_mode, int cur, long long* bu_out) {
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   const bool all = cand_mode == 0 || w->sc.include_idle;
   if (M <= EC_TSIZE) {
     const int i = EC_LANE + 1;
@@ -1836,7 +1844,7 @@ template <class W>
 EC_COLD1 void job_deps(W* w, const GP& g, int tid, int nthr) {
   (void)g;
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances, n_dep = w->n_dep, stop_p = w->j_stop;
+  const int M = ec_nm(w), n_dep = w->n_dep, stop_p = w->j_stop;
   for (int x = tid; x < n_dep * M; x += nthr) {
     const int k = x / M, i = x - k * M + 1;
     const int dp = w->dep_pos[k];
@@ -1903,7 +1911,7 @@ template <class W, int RCAP>
 EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   const AsbScenario& sc = w->sc;
   if (sc.interference > 0) return false;
-  const int M = sc.n_instances;
+  const int M = ec_nm(w);
   EC_WPROF_START(w);
   /* ---- step 0: the rank sort already ordered exact ties by push seq; an
    * unknown seq inside a tie needs the serial walk */
@@ -2393,7 +2401,7 @@ template <class W>
 EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   (void)g;
   const int n_all = w->n_rec;
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   const int lane = tid & 31, wid = tid >> 5;
   ulonglong2* key = reinterpret_cast<ulonglong2*>(w->skey);
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
@@ -2508,7 +2516,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
 template <class W>
 EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
-  const int M = w->sc.n_instances;
+  const int M = ec_nm(w);
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
   for (int j = tid; j < n_all; j += nthr) {
@@ -2992,7 +3000,7 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
 template <class W, int RCAP, int DCAP, int ACAP, bool TS>
 EC_DEV void run_scenario(W* w, const GP& g) {
   const AsbScenario& sc = w->sc;
-  const int M = sc.n_instances, L = sc.n_levels;
+  const int M = ec_nm(w), L = sc.n_levels;
   /* ---- init (engine.py:251-276) */
   fork_job(w, JOB_INIT);
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
