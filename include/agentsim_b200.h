@@ -245,7 +245,9 @@ size_t asb_workspace_bytes(int32_t n_scen, int64_t total_agents, int64_t total_r
 
 /* Run all scenarios to completion (one CTA team per scenario, persistent grid).
  * d_scen: device array of n_scen AsbScenario; max_instances = max
- * n_instances over the batch (<= 64). */
+ * n_instances over the batch (<= 64), or -m when every scenario of the batch
+ * has exactly m instances (the launcher then picks a kernel whose instance
+ * count is a compile-time constant). */
 int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_instances,
                       AsbTracePool traces, AsbTablePool tables, AsbOutputs out,
                       int64_t total_agents, int64_t total_ring_slots, void* d_workspace,

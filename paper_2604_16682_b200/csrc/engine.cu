@@ -373,7 +373,7 @@ int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp,
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
   static_assert(NT % 32 == 0 && NT >= 32 && (NT & (NT - 1)) == 0, "team = a power-of-two number of whole warps");
   /* 4 teams per SM need <= ~54 KB of shared memory each (228 KB per SM) */
-  static_assert(NT > 128 || MAXM > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
+  static_assert(NT > 128 || W::MX > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
   const size_t smem = (sizeof(W) + 15) / 16 * 16;
   auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -417,6 +417,8 @@ size_t asb_workspace_bytes(int32_t n_scen, int64_t total_agents, int64_t total_r
 int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_instances, AsbTracePool traces,
                       AsbTablePool tables, AsbOutputs out, int64_t total_agents, int64_t total_ring_slots,
                       void* d_workspace, size_t workspace_bytes, void* stream) {
+  const bool fixed_m = max_instances < 0; /* -m: every scenario has exactly m instances */
+  if (fixed_m) max_instances = -max_instances;
   if (n_scen < 0 || max_instances < 1 || max_instances > 64) return ASB_ERR_ARG;
   if (out.timeseries && (!out.ts_off || !out.ts_count)) return ASB_ERR_ARG; /* rows need their offsets and counts */
   if (n_scen == 0) return ASB_OK;
@@ -458,6 +460,9 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   if (max_instances == 1 && solo) return launch_engine<1, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16) {
     if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
+    /* every scenario with exactly 16 instances (the Monte-Carlo sweep): the
+     * count is a compile-time constant */
+    if (fixed_m && max_instances == 16 && !getenv("ASB_NO_FIXED_M")) return launch_engine<-16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   }
   if (solo) return launch_engine<64, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);

@@ -235,7 +235,10 @@ struct WS {
   static constexpr int NT = NTHR;          /* threads of the team (main warp + helpers) */
   static constexpr int NW = (NTHR + 31) / 32;
   static constexpr int RC = RCAP, DC = DCAP, AC = ACAP;
-  static constexpr int MX = MAXM;          /* instance capacity of the kernel */
+  /* instance capacity of the kernel; a negative MAXM: every scenario of
+   * the launch has exactly -MAXM instances (a compile-time count) */
+  static constexpr int MX = MAXM < 0 ? -MAXM : MAXM;
+  static constexpr bool FIXM = MAXM < 0;
   /* large-batch teams: more dependent records per walk, and the apply
    * reloads agent state instead of caching it in shared memory */
   static constexpr int DEP = RCAP >= 512 ? 64 : EC_DEPCAP;
@@ -266,7 +269,7 @@ struct WS {
   };
   unsigned char depflag[RCAP];
   short ki[RCAP], kir[RCAP], krank[RCAP], ilist[RCAP]; /* per-instance record lists */
-  int icnt[MAXM], ioff[MAXM + 1];
+  int icnt[MX], ioff[MX + 1];
   double now, bound;
   long long seq, start_ctr;
   long long ctr[ASB_NCOUNTERS];
@@ -278,15 +281,15 @@ struct WS {
   int due_ready, n_cand, cand_token, n_empty, cand_collect;
   int stamp_ctr; /* last due-list stamp handed out (dstamp de-duplication) */
   double pr[16], dr[16], act[16], idle[16];
-  Inst in[MAXM];
-  unsigned long long tmin[MAXM];
+  Inst in[MX];
+  unsigned long long tmin[MX];
   /* epoch scratch (per instance) */
-  long long ep_uobs[MAXM], ep_seq[MAXM];
-  double ep_mintp[MAXM];
-  int ep_level[MAXM], ep_boost[MAXM], ep_nadm[MAXM], ep_head[MAXM], ep_retime[MAXM], ep_def[MAXM], ep_thr0[MAXM];
-  int ep_nstart[MAXM];
-  long long ep_rank[MAXM];
-  int ep_list[MAXM];
+  long long ep_uobs[MX], ep_seq[MX];
+  double ep_mintp[MX];
+  int ep_level[MX], ep_boost[MX], ep_nadm[MX], ep_head[MX], ep_retime[MX], ep_def[MX], ep_thr0[MX];
+  int ep_nstart[MX];
+  long long ep_rank[MX];
+  int ep_list[MX];
   int n_eplist;
   double ep_gcap;
   int due[DCAP];
@@ -302,7 +305,7 @@ struct WS {
   int dep_pos[DEP];
   int dep_target[DEP]; /* routed instance of each dependent arrival; -1: a migrating check (JOB_DEPS) */
   int j_stop;          /* JOB_DEPS: records at or after this position are not committed */
-  long long snap[DEP][MAXM];
+  long long snap[DEP][MX];
   long long carry_u;
   int carry_r, carry_l;
   unsigned wmask[(RCAP + 31) / 32]; /* power-change entries of the scan walk, one bit per ilist entry */
@@ -311,15 +314,15 @@ struct WS {
   long long prof_t;
   /* timeseries: rows written, next sample index, each instance's last row */
   long long ts_n, ts_k;
-  long long ts_last[MAXM];
+  long long ts_last[MX];
 };
 
-/* the scenario's instance count; a compile-time 1 in the single-instance
- * kernels (MAXM = 1), so that their per-instance loops, scans and argmins
- * fold away */
+/* the scenario's instance count; a compile-time constant in the
+ * single-instance kernels (MAXM = 1) and the fixed-count kernels (MAXM < 0),
+ * so that their per-instance loops, scans and argmins fold away */
 template <class W>
 EC_DEV int ec_nm(const W* w) {
-  return W::MX == 1 ? 1 : w->sc.n_instances;
+  return (W::FIXM || W::MX == 1) ? W::MX : w->sc.n_instances;
 }
 
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase

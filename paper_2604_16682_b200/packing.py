@@ -245,10 +245,17 @@ class Batch:
     total_agents: int
     total_ring: int
     max_instances: int
+    min_instances: int = 0
 
     @property
     def n(self) -> int:
         return int(self.scen.size)
+
+    @property
+    def launch_instances(self) -> int:
+        """asb_run_scenarios' max_instances argument: -m when every scenario
+        has exactly m instances (a fixed-count kernel), else the maximum."""
+        return -self.max_instances if self.min_instances == self.max_instances else self.max_instances
 
 
 def build_batch(scen: np.ndarray, traces: TracePool, tables: TablePool) -> Batch:
@@ -277,4 +284,5 @@ def build_batch(scen: np.ndarray, traces: TracePool, tables: TablePool) -> Batch
         total_agents=int(a_cnt.sum()),
         total_ring=int((m * a_cnt).sum()),
         max_instances=int(m.max()) if n else 1,
+        min_instances=int(m.min()) if n else 1,
     )
