@@ -93,6 +93,18 @@ EC_DEV double ec_floor(double x) { return floor(x); }
 EC_DEV unsigned long long ec_bits(double x) { return (unsigned long long)__double_as_longlong(x); }
 EC_DEV double ec_from_bits(unsigned long long b) { return __longlong_as_double((long long)b); }
 EC_DEV long long ec_clock() { return clock64(); }
+#ifdef ASB_PROFILE_PLACEMENT
+EC_DEV long long ec_smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+EC_DEV long long ec_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+#endif
 EC_DEV float ec_f32_down(double x) { return __double2float_rd(x); } /* rounded toward -inf: <= x */
 #define EC_INF_F32 __int_as_float(0x7f800000)
 /* a team is NT consecutive threads (NT a power of two): one team per CTA */

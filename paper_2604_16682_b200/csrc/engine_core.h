@@ -3004,6 +3004,9 @@ template <class W, int RCAP, int DCAP, int ACAP, bool TS>
 EC_DEV void run_scenario(W* w, const GP& g) {
   const AsbScenario& sc = w->sc;
   const int M = ec_nm(w), L = sc.n_levels;
+#ifdef ASB_PROFILE_PLACEMENT
+  EC_LANE0 w->prof_t = ec_globaltimer();
+#endif
   /* ---- init (engine.py:251-276) */
   fork_job(w, JOB_INIT);
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
@@ -3118,6 +3121,12 @@ EC_DEV void run_scenario(W* w, const GP& g) {
     w->ctr[ASB_CTR_STATUS] = w->status;
 #ifdef ASB_PROFILE
     for (int c = 0; c < 6; c++) w->ctr[10 + c] = w->prof[c];
+#endif
+#ifdef ASB_PROFILE_PLACEMENT
+    /* experiment: where and when the scenario ran (SM id, global ns) */
+    w->ctr[10] = ec_smid();
+    w->ctr[11] = w->prof_t;
+    w->ctr[12] = ec_globaltimer();
 #endif
     for (int c = 0; c < ASB_NCOUNTERS; c++) g.o_ctr[c] = w->ctr[c];
   }
