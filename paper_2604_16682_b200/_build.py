@@ -63,7 +63,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
     srcs = [os.path.join(CSRC, f) for f in ("engine.cu", "unit_ops.cu")]
     deps = srcs + [os.path.join(CSRC, "engine_core.h"), os.path.join(ROOT, "include", "agentsim_b200.h")]
     target = {"walk": WPROF_LIB_PATH, "debug": DEBUG_LIB_PATH,
-              "sweep": os.path.join(LIB_DIR, "libagentsim_b200_sprof.so")}.get(profile) if isinstance(profile, str) else (
+              "sweep": os.path.join(LIB_DIR, "libagentsim_b200_sprof.so"),
+              "sort": os.path.join(LIB_DIR, "libagentsim_b200_qprof.so")}.get(profile) if isinstance(profile, str) else (
         PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
@@ -76,6 +77,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
             cmd.insert(1, "-DASB_PROFILE_WALK")
         if profile == "sweep":
             cmd.insert(1, "-DASB_PROFILE_SWEEP")
+        if profile == "sort":
+            cmd.insert(1, "-DASB_PROFILE_SORT")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)

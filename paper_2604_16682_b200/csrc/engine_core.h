@@ -100,6 +100,9 @@
 #endif
 /* loops over instances: kept rolled, the trip count is small and the
  * co-resident teams share a 32 KB instruction cache */
+#ifndef EC_BITONIC_MIN
+#define EC_BITONIC_MIN 256 /* the 16-warp team bitonic-sorts batches of more records than this */
+#endif
 #ifndef EC_ILOOP
 #define EC_ILOOP _Pragma("unroll 1")
 #endif
@@ -243,6 +246,9 @@ struct WS {
    * reloads agent state instead of caching it in shared memory */
   static constexpr int DEP = RCAP >= 512 ? 64 : EC_DEPCAP;
   static constexpr bool CC = RCAP < 512;
+  /* the 16-warp team's sort: horizon cut and per-instance lists by the
+   * whole team (the smaller teams keep the shorter warp-0 code) */
+  static constexpr bool BIGSORT = NTHR >= 512;
   AsbScenario sc;
   GP gp;                                   /* shared with the helper warps */
   /* fork-join job state */
@@ -266,6 +272,9 @@ struct WS {
       long long wu[RCAP];
       int wr[RCAP], wl[RCAP];
     };
+    /* rank sort, after the keys: per 32-record chunk of the sorted order and
+     * per instance, its record count, then the count in earlier chunks */
+    unsigned short kcc[(RCAP + 31) / 32][MX];
   };
   unsigned char depflag[RCAP];
   short ki[RCAP], kir[RCAP], krank[RCAP], ilist[RCAP]; /* per-instance record lists */
@@ -325,6 +334,27 @@ EC_DEV int ec_nm(const W* w) {
   return (W::FIXM || W::MX == 1) ? W::MX : w->sc.n_instances;
 }
 
+/* optional sort timing (-DASB_PROFILE -DASB_PROFILE_SORT): thread 0's
+ * cycles per JOB_SORT step in prof[0..5] */
+#if defined(ASB_PROFILE_SORT)
+#define EC_QPROF_T0() long long qprof_t_ = ec_clock()
+#define EC_QPROF(w, k)                               \
+  do {                                               \
+    if (tid == 0) {                                  \
+      const long long qn_ = ec_clock();              \
+      (w)->prof[k] += qn_ - qprof_t_;                \
+      qprof_t_ = qn_;                                \
+    }                                                \
+  } while (0)
+#else
+#define EC_QPROF_T0() \
+  do {                \
+  } while (0)
+#define EC_QPROF(w, k) \
+  do {                 \
+  } while (0)
+#endif
+
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
  * accumulated by lane 0 and reported in counters[10..15];
  * -DASB_PROFILE -DASB_PROFILE_WALK times the commit-walk steps instead */
@@ -369,7 +399,7 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_PROF(w, k) \
   do {                \
   } while (0)
-#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP)
+#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT)
 #define EC_WPROF_START(w) \
   do {                    \
   } while (0)
@@ -2406,19 +2436,18 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   const int n_all = w->n_rec;
   const int M = ec_nm(w);
   const int lane = tid & 31, wid = tid >> 5;
+  EC_QPROF_T0();
   ulonglong2* key = reinterpret_cast<ulonglong2*>(w->skey);
-  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
-  for (int i = tid; i < M; i += nthr) w->icnt[i] = 0;
   auto emit = [&](int j, int rank, unsigned long long tj) {
     const Rec& rr = w->rec[j];
     const bool empty = rr.flags & F_EMPTY;
     const unsigned pj = empty ? 0xffu : (unsigned)rr.prio;
     sort_emit(w, j, rank, empty ? ~0ull : tj, pj);
     w->ki[rank] = (short)(empty || pj == EV_ARRIVAL ? 0 : rr.inst); /* by rank */
-    if (!empty && !below_horizon(tj, pj, rr.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s))
+    if (!W::BIGSORT && !empty && !below_horizon(tj, pj, rr.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s))
       t_atomic_min_i(&w->j_cut, rank);
   };
-  if (W::NT >= 512 && n_all > 256) {
+  if (W::NT >= 512 && n_all > EC_BITONIC_MIN) {
     /* the 16-warp team's batches of more than 256 records: a bitonic sort
      * of the keys (the record index sits in the low 11 bits of the second
      * half), O(n log^2 n) steps instead of the counting rank's O(n^2)
@@ -2430,6 +2459,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
       key[j] = make_ulonglong2(k.k1, k.k2);
     }
     ec_team_barrier(W::NT);
+    EC_QPROF(w, 0);
     for (int k = 2; k <= N; k <<= 1) {
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
         for (int i = tid; i < N; i += nthr) {
@@ -2446,16 +2476,19 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
         ec_team_barrier(W::NT);
       }
     }
+    EC_QPROF(w, 1);
     for (int p = tid; p < n_all; p += nthr) {
       const ulonglong2 kp = key[p];
       emit((int)(kp.y & 0x7ffull), p, kp.x);
     }
+    EC_QPROF(w, 2);
   } else {
   for (int j = tid; j < n_all; j += nthr) {
     const SKey k = skey_of(w, j, n_all);
     key[j] = make_ulonglong2(k.k1, k.k2);
   }
   ec_team_barrier(W::NT);
+  EC_QPROF(w, 0);
   for (int j = tid; j < n_all; j += nthr) {
     const ulonglong2 me = key[j];
     int rank = 0;
@@ -2474,45 +2507,118 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     }
     emit(j, rank, me.x);
   }
+  EC_QPROF(w, 2);
   }
   ec_team_barrier(W::NT);
-  /* exact (time, prio) ties with an unknown push seq need the serial walk */
+  EC_QPROF(w, 3);
+  /* exact (time, prio) ties with an unknown push seq need the serial walk;
+   * the horizon cut: records at or beyond the horizon key form a suffix of
+   * the non-empty sorted records (the key orders like (time, prio, seq)),
+   * whose first position is the cut (one writer, no atomics) */
   int tie_unknown = 0;
-  for (int p = tid + 1; p < n_all; p += nthr) {
-    if (w->sw_prio[p] == 0xff) continue;
-    if (w->srt[p].tb == w->srt[p - 1].tb && w->sw_prio[p] == w->sw_prio[p - 1] &&
-        (w->rec[w->sw_idx[p]].seq < 0 || w->rec[w->sw_idx[p - 1]].seq < 0))
-      tie_unknown = 1;
+  if (!W::BIGSORT) {
+    for (int p = tid + 1; p < n_all; p += nthr) {
+      if (w->sw_prio[p] == 0xff) continue;
+      if (w->srt[p].tb == w->srt[p - 1].tb && w->sw_prio[p] == w->sw_prio[p - 1] &&
+          (w->rec[w->sw_idx[p]].seq < 0 || w->rec[w->sw_idx[p - 1]].seq < 0))
+        tie_unknown = 1;
+    }
+    if (tie_unknown) w->j_tie_unknown = 1;
+    EC_QPROF(w, 4);
+    /* per-instance lists of sorted positions, in rank order (warp 0) */
+    if (wid == 0) {
+      EC_ILOOP /* per-instance loop: rolled (instruction cache) */
+      for (int i = lane; i < M; i += 32) w->icnt[i] = 0;
+      __syncwarp();
+      for (int base = 0; base < n_all; base += 32) {
+        const int p = base + lane;
+        const int ij = p < n_all ? w->ki[p] : 0;
+        const unsigned peers = __match_any_sync(0xffffffffu, ij);
+        const int before = __popc(peers & t_lt_mask());
+        if (ij) w->krank[p] = (short)(w->icnt[ij - 1] + before); /* position in instance ij's list */
+        __syncwarp();
+        if (ij && before == 0) w->icnt[ij - 1] += __popc(peers);
+        __syncwarp();
+      }
+      long long run = 0;
+      EC_ILOOP /* per-instance loop: rolled (instruction cache) */
+      for (int base = 0; base < M; base += 32) {
+        const int i = base + lane;
+        const long long c = i < M ? w->icnt[i] : 0;
+        const long long inc = t_scan_add_ll(c);
+        if (i < M) w->ioff[i] = (int)(run + inc - c);
+        run += t_bcast_ll(inc, 31);
+      }
+      if (lane == 0) w->ioff[M] = (int)run;
+      __syncwarp();
+      for (int p = lane; p < n_all; p += 32) {
+        const int ij = w->ki[p];
+        if (ij) w->ilist[w->ioff[ij - 1] + w->krank[p]] = (short)p;
+      }
+    }
+    EC_QPROF(w, 5);
+    return;
+  }
+  const unsigned long long hzt = w->hz_t;
+  const unsigned hzp = (unsigned)w->hz_p;
+  const long long hzs = w->hz_s;
+  for (int p = tid; p < n_all; p += nthr) {
+    const unsigned pp = w->sw_prio[p];
+    if (pp == 0xff) continue;
+    const unsigned long long tb = w->srt[p].tb;
+    const long long sq = w->rec[w->sw_idx[p]].seq;
+    if (p > 0) {
+      const unsigned long long tb1 = w->srt[p - 1].tb;
+      const unsigned pp1 = w->sw_prio[p - 1];
+      const long long sq1 = w->rec[w->sw_idx[p - 1]].seq;
+      if (tb == tb1 && pp == pp1 && (sq < 0 || sq1 < 0)) tie_unknown = 1;
+      if (!below_horizon(tb, pp, sq, hzt, hzp, hzs) && below_horizon(tb1, pp1, sq1, hzt, hzp, hzs)) w->j_cut = p;
+    } else if (!below_horizon(tb, pp, sq, hzt, hzp, hzs)) {
+      w->j_cut = 0;
+    }
   }
   if (tie_unknown) w->j_tie_unknown = 1;
-  /* per-instance lists of sorted positions, in rank order (warp 0) */
+  EC_QPROF(w, 4);
+  /* per-instance lists of sorted positions, in rank order, by the whole
+   * team: each warp counts its 32-record chunks per instance (match_any),
+   * warp 0 turns the chunk counts into offsets, then every record is placed */
+  const int nch = (n_all + 31) >> 5;
+  for (int c = wid; c < nch; c += W::NW) {
+    EC_ILOOP /* per-instance loop: rolled (instruction cache) */
+    for (int i = lane; i < M; i += 32) w->kcc[c][i] = 0;
+    __syncwarp();
+    const int p = (c << 5) + lane;
+    const int ij = p < n_all ? w->ki[p] : 0;
+    const unsigned peers = __match_any_sync(0xffffffffu, ij);
+    const int before = __popc(peers & t_lt_mask());
+    if (ij) w->krank[p] = (short)before; /* position among the chunk's records on ij */
+    if (ij && before == 0) w->kcc[c][ij - 1] = (unsigned short)__popc(peers);
+  }
+  ec_team_barrier(W::NT);
   if (wid == 0) {
-    for (int base = 0; base < n_all; base += 32) {
-      const int p = base + lane;
-      const int ij = p < n_all ? w->ki[p] : 0;
-      const unsigned peers = __match_any_sync(0xffffffffu, ij);
-      const int before = __popc(peers & t_lt_mask());
-      if (ij) w->krank[p] = (short)(w->icnt[ij - 1] + before); /* position in instance ij's list */
-      __syncwarp();
-      if (ij && before == 0) w->icnt[ij - 1] += __popc(peers);
-      __syncwarp();
-    }
     long long run = 0;
     EC_ILOOP /* per-instance loop: rolled (instruction cache) */
     for (int base = 0; base < M; base += 32) {
       const int i = base + lane;
-      const long long c = i < M ? w->icnt[i] : 0;
-      const long long inc = t_scan_add_ll(c);
-      if (i < M) w->ioff[i] = (int)(run + inc - c);
+      int cnt = 0;
+      if (i < M)
+        for (int c = 0; c < nch; c++) {
+          const int t = w->kcc[c][i];
+          w->kcc[c][i] = (unsigned short)cnt;
+          cnt += t;
+        }
+      const long long inc = t_scan_add_ll(cnt);
+      if (i < M) w->ioff[i] = (int)(run + inc - cnt);
       run += t_bcast_ll(inc, 31);
     }
     if (lane == 0) w->ioff[M] = (int)run;
-    __syncwarp();
-    for (int p = lane; p < n_all; p += 32) {
-      const int ij = w->ki[p];
-      if (ij) w->ilist[w->ioff[ij - 1] + w->krank[p]] = (short)p;
-    }
   }
+  ec_team_barrier(W::NT);
+  for (int p = tid; p < n_all; p += nthr) {
+    const int ij = w->ki[p];
+    if (ij) w->ilist[w->ioff[ij - 1] + w->kcc[p >> 5][ij - 1] + w->krank[p]] = (short)p;
+  }
+  EC_QPROF(w, 5);
 }
 #else
 /* JOB_SORT, generic team (the 1-lane host harness): O(n^2) rank sort */
@@ -2871,7 +2977,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   EC_PROF(w, 2);
-#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP)
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT)
   EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
   t_sync();
 #endif
