@@ -2,20 +2,23 @@
 """bench.py — agent-ticks/s of the batched scenario engine on B200.
 
 Workload (default, BASELINE.json configs[4] "C5"): the
-Monte-Carlo sweep sharded across GPUs — per GPU 512 scenarios = 64 seeds x 8
-cells {router context_aware|round_robin} x {controller context_aware|off} x
-{SLO tau 20|35}; each scenario 16 instances x ~10k agents (WorkloadSpec
-arrival_rate=10000/3600, 3600 s), 3600 control epochs.  Weak scaling: rank r
-simulates seeds [64r, 64r+64).  One step = every scenario of the shard run to
-completion (engine kernel + per-scenario stats + stats fold), plus the NCCL
-allreduce of the 8-double stats vector when N > 1.
+Monte-Carlo sweep, 4096 scenarios = 512 seeds x 8 cells {router
+context_aware|round_robin} x {controller context_aware|off} x {SLO tau 20|35};
+each scenario 16 instances x ~10k agents (WorkloadSpec arrival_rate=10000/3600,
+3600 s), 3600 control epochs.  The whole job fits one B200, so N=1 runs all of
+it; at N GPUs rank r takes seeds [512r/N, 512(r+1)/N) (strong scaling: the job
+is fixed, N=8 is the 512-scenario-per-GPU split BASELINE names).  One step =
+every scenario of the rank's share run to completion (engine kernel +
+per-scenario stats + stats fold), plus the NCCL allreduce of the 8-double
+stats vector when N > 1.  `--config c5` keeps the fixed 512-scenario shard per
+GPU (weak scaling).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config c5|c3|c4]
+  python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference] [--config c5full|c5|c3|c4]
 
 --config selects another BASELINE.json workload for the same line format:
 c3 = the DVFS sweep (8 fixed levels x 4 capacities x 64 seeds per GPU, 1
 instance x ~1k agents, 12500 epochs), c4 = the 100k-agent thrashing regime
-(one scenario, 64 instances).  The driver's headline is the default (c5).
+(one scenario, 64 instances).  The driver's headline is the default (c5full).
 
 `--impl reference` times the CPU restatement of the reference (oracle/,
 serial C DES, OpenMP over scenarios on all host cores) on the same shard.
@@ -48,8 +51,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("b200", "reference"), default="b200")
-    p.add_argument("--config", choices=tuple(CONFIGS), default="c5",
-                   help="workload (BASELINE.json configs): c5 = the headline Monte-Carlo shard")
+    p.add_argument("--config", choices=tuple(CONFIGS), default="c5full",
+                   help="workload (BASELINE.json configs): c5full = the headline Monte-Carlo sweep, all 4096 "
+                        "scenarios split over the GPUs (strong scaling); c5 = a fixed 512-scenario shard per GPU")
     p.add_argument("--seeds-per-gpu", type=int, default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")

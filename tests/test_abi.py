@@ -36,3 +36,18 @@ def test_workspace_size_is_monotone():
     a = lib.asb_workspace_bytes(4, 1000, 16000)
     b = lib.asb_workspace_bytes(4, 2000, 32000)
     assert 0 < a < b
+
+
+def test_launch_instances_declares_fixed_counts():
+    """asb_run_scenarios' max_instances: -m when every scenario has m
+    instances (fixed-count kernels), else the maximum (include/agentsim_b200.h)."""
+    import dataclasses
+
+    import paper_2604_16682_b200 as asb
+    from paper_2604_16682_b200.engine import prepare_batch
+
+    traces = asb.generate_workload(asb.WorkloadSpec(arrival_rate=0.2, duration=30.0, seed=1))
+    base = asb.SimConfig(traces=traces, instance_count=4, sim_duration=40.0)
+    assert prepare_batch([base, base]).launch_instances == -4
+    assert prepare_batch([base, dataclasses.replace(base, instance_count=1)]).launch_instances == 4
+    assert prepare_batch([dataclasses.replace(base, instance_count=1)]).launch_instances == -1

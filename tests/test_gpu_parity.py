@@ -207,3 +207,51 @@ def test_large_tie_storm_batches(cuda_device, team):
     want, wst = run_oracle(batch)
     diff = array_outputs_equal(want, got)
     assert diff is None, diff
+
+
+def _with_instances(cfgs, m):
+    import dataclasses
+
+    return [dataclasses.replace(c, instance_count=m) for c in cfgs]
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_single_instance_kernel_matches_oracle(cuda_device, seed):
+    """Every scenario single-instance: the batch runs the kernel whose
+    instance count is the compile-time 1 (asb_run_scenarios(-1)), across all
+    controller variants, interference, thrash avoidance and tie storms."""
+    batch = prepare_batch(_with_instances(_random_configs(seed, 96), 1))
+    assert batch.launch_instances == -1
+    got, gst = gpu(batch)
+    want, wst = run_oracle(batch)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
+    for f in _abi.STATS_DTYPE.names:
+        assert np.array_equal(gst[f], wst[f], equal_nan=True), f
+
+
+@pytest.mark.parametrize("seed,team", [(23, "quad"), (24, "solo"), (25, "big")], indirect=["team"])
+def test_fixed_count_kernel_matches_oracle(cuda_device, seed, team, monkeypatch):
+    """Every scenario with 16 instances: the quad team runs the kernel whose
+    instance count is the compile-time 16; the result equals the oracle and
+    the run-time-count kernel's (ASB_NO_FIXED_M) bit for bit."""
+    batch = prepare_batch(_with_instances(_random_configs(seed, 48), 16))
+    assert batch.launch_instances == -16
+    got, gst = gpu(batch)
+    want, wst = run_oracle(batch)
+    diff = array_outputs_equal(want, got)
+    assert diff is None, diff
+    monkeypatch.setenv("ASB_NO_FIXED_M", "1")
+    got2, _ = gpu(batch)
+    assert array_outputs_equal(got, got2) is None
+
+
+def test_mixed_instance_counts_take_the_general_kernel(cuda_device):
+    """A batch mixing instance counts passes the maximum (not -m) and matches
+    the oracle."""
+    cfgs = _with_instances(_random_configs(26, 16), 16) + _with_instances(_random_configs(27, 16), 3)
+    batch = prepare_batch(cfgs)
+    assert batch.launch_instances == 16
+    got, _ = gpu(batch)
+    want, _ = run_oracle(batch)
+    assert array_outputs_equal(want, got) is None

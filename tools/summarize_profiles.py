@@ -59,10 +59,12 @@ def raw_metrics(rep):
 
 def main():
     tag = sys.argv[1]
+    config = sys.argv[2] if len(sys.argv) > 2 else "c5full"  # the workload of the captured launch
     src = os.path.join(ROOT, "gpurun_out", tag)
     dst = os.path.join(ROOT, "profiles", tag)
     os.makedirs(dst, exist_ok=True)
-    for f in ("bench.json", "pytest_gpu.log", "smoke.log", "gpu.txt", "phases.json", "phases_walk.json"):
+    for f in ("bench.json", "bench_ref.json", "bench_c3.json", "bench_c4.json", "bench_c5.json", "batch_api.json",
+              "pytest_gpu.log", "smoke.log", "gpu.txt", "phases.json", "phases_walk.json"):
         if os.path.exists(os.path.join(src, f)):
             shutil.copy(os.path.join(src, f), os.path.join(dst, f))
     if os.path.exists(os.path.join(src, "launches.csv")):
@@ -82,13 +84,13 @@ def main():
         top = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_lines.py"), tmp, "60"],
                              capture_output=True, text=True).stdout
         open(os.path.join(dst, "ncu_engine_full.txt"), "w").write(
-            "ncu --set full --clock-control none --import-source on -k regex:asb_engine (1 launch, C5 shard)\n\n"
+            f"ncu --set full --clock-control none --import-source on -k regex:asb_engine (1 launch, bench --config {config})\n\n"
             + "\n".join(txt) + "\n\nTop source lines by warp-stall samples:\n" + top)
         d = mets[0]
         scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}
         rd = float(d["dram__bytes_read.sum"][0].replace(",", "")) * scale[d["dram__bytes_read.sum"][1]]
         wr = float(d["dram__bytes_write.sum"][0].replace(",", "")) * scale[d["dram__bytes_write.sum"][1]]
-        traffic = {"tag": tag, "config": "c5", "kernel": "asb_engine_kernel", "dram_bytes_per_launch": rd + wr,
+        traffic = {"tag": tag, "config": config, "kernel": "asb_engine_kernel", "dram_bytes_per_launch": rd + wr,
                    "dram_read": rd, "dram_write": wr, "source": f"profiles/{tag}/ncu_engine_full.txt"}
         json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_engine_traffic.json"), "w"), indent=1)
     print("wrote", dst)
