@@ -2049,8 +2049,13 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
    * one binary search per (record, instance) pair across the lanes; many
    * instances (M > 32): lane per instance, merging its sorted record list
    * with the sorted dependent positions */
-  const bool team_deps = W::NW > 1 && n_dep > 0 && (M > EC_TSIZE ? W::MX > 32 : EC_TEAM_DEPS_SMALL);
-  if (team_deps) {
+  /* a single instance (compile-time): every arrival routes to it and no
+   * reassignment can migrate (the argmin is the current instance,
+   * router.py:110-128), so no snapshots or checks are needed */
+  constexpr bool single = W::MX == 1;
+  const bool team_deps = !single && W::NW > 1 && n_dep > 0 && (M > EC_TSIZE ? W::MX > 32 : EC_TEAM_DEPS_SMALL);
+  if (single) {
+  } else if (team_deps) {
     /* many instances, helper warps: snapshots, checks and routing as a team job */
     EC_LANE0 w->j_stop = stop_p;
     t_sync();
@@ -2084,8 +2089,8 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     snapshots_merge(w, n_dep, stop_p);
   }
   t_sync();
-  if (team_deps) {
-    /* done by JOB_DEPS */
+  if (single || team_deps) {
+    /* nothing to check / done by JOB_DEPS */
   } else if (EC_WIDE_LANE_PAR && M > EC_TSIZE) {
     /* many instances: one lane per check */
     if (n_dep > 0) {
@@ -2202,7 +2207,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
   t_sync();
   EC_WPROF(w, 4);
   /* ---- step 5: arrivals in order (routing on the usage snapshot) */
-  if (team_deps) {
+  if (team_deps || single) {
     /* many instances, routed by JOB_DEPS: commit the arrivals a lane each
      * (_on_arrival bookkeeping, engine.py:490-507, as commit_arrival does
      * it one by one): arrival rank, alive slot and arrival_rank from the
@@ -2221,8 +2226,9 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
         const Rec& r = w->rec[w->sw_idx[p]];
         a = r.agent;
         order_pos = (int)r.seq;
-        target = sc.policy == ASB_POLICY_ROUND_ROBIN ? (int)(((long long)w->rr_next + rank) % M) + 1
-                                                     : w->dep_target[k];
+        target = single ? 1
+                 : sc.policy == ASB_POLICY_ROUND_ROBIN ? (int)(((long long)w->rr_next + rank) % M) + 1
+                                                       : w->dep_target[k];
       }
       const unsigned peers = t_match_any_i(arr ? target : 0) & m;
       const int same_before = ec_popc(peers & t_lt_mask());
