@@ -469,7 +469,11 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   /* single-instance scenarios (the DVFS sweep): a kernel whose instance
    * count is the constant 1, with the per-instance machinery folded away */
-  if (max_instances == 1 && solo) return launch_engine<1, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
+#ifndef ASB_SOLO1_RC
+#define ASB_SOLO1_RC 64 /* 64-record batches: fewer window splits, still 14 teams per SM (15.5 KB) */
+#endif
+  if (max_instances == 1 && solo)
+    return launch_engine<1, ASB_SOLO1_RC, ASB_SOLO1_RC / 2, ASB_SOLO1_RC / 2, 32>(d_scen, n_scen, traces, tables, out, ws, st);
   if (max_instances <= 16) {
     if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
     /* every scenario with exactly 16 instances (the Monte-Carlo sweep): the
