@@ -37,7 +37,11 @@ def main():
     t0 = time.perf_counter()
     db.run()
     torch.cuda.synchronize()
-    out["device_run_s"] = time.perf_counter() - t0
+    out["device_run_s"] = time.perf_counter() - t0  # first launch: module load + 1.4 GB of decision rows
+    t0 = time.perf_counter()
+    db.run()
+    torch.cuda.synchronize()
+    out["device_rerun_s"] = time.perf_counter() - t0
     t0 = time.perf_counter()
     host, stats = db.download()
     out["download_s"] = time.perf_counter() - t0
