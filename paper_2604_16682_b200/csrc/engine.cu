@@ -42,6 +42,9 @@
 #endif
 #define EC_COLD4 __device__ __noinline__
 #define EC_LANE ((int)(threadIdx.x & 31))
+#ifndef ASB_NO_PREFETCH
+#define EC_PREFETCH_L2(p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p))
+#endif
 #define EC_TSIZE 32
 #define EC_NAN __longlong_as_double(0x7ff8000000000000ll)
 #define EC_INF __longlong_as_double(0x7ff0000000000000ll)

@@ -103,6 +103,9 @@
 #ifndef EC_BITONIC_MIN
 #define EC_BITONIC_MIN 256 /* the 16-warp team bitonic-sorts batches of more records than this */
 #endif
+#ifndef EC_PREFETCH_L2
+#define EC_PREFETCH_L2(p) ((void)(p))
+#endif
 #ifndef EC_ILOOP
 #define EC_ILOOP _Pragma("unroll 1")
 #endif
@@ -1146,6 +1149,10 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
           const int pos = t_atomic_add_i(&w->j_total, 1);
           if (pos < W::DC) w->due[pos] = a;
           g.dstamp[a] = token;
+          /* the speculation reads this agent's record and turn offsets after
+           * the epoch: start bringing them into L2 now */
+          EC_PREFETCH_L2(&g.H[a]);
+          EC_PREFETCH_L2(&g.aturn[a]);
         }
       }
       if (!tick) continue;
