@@ -408,13 +408,22 @@ def main():
     from paper_2604_16682_b200.parallel import allreduce_stats
 
     _build.build_cuda()
+    # ASB_DIST_BACKEND=gloo: a functional check of the multi-rank path on a
+    # box with fewer GPUs than ranks (ranks share devices; timings are not
+    # scaling numbers).  The benchmark itself is one rank per GPU over NCCL.
+    backend = os.environ.get("ASB_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
     batch, seeds = build_shard(rank, args.seeds_per_gpu, args.config)
     db = DeviceBatch(batch, device=dev)
