@@ -2463,35 +2463,75 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
     if (!W::BIGSORT && !empty && !below_horizon(tj, pj, rr.seq, w->hz_t, (unsigned)w->hz_p, w->hz_s))
       t_atomic_min_i(&w->j_cut, rank);
   };
-  if (W::NT >= 512 && n_all > EC_BITONIC_MIN) {
+  if (W::NT == 512 && n_all > EC_BITONIC_MIN) {
     /* the 16-warp team's batches of more than 256 records: a bitonic sort
      * of the keys (the record index sits in the low 11 bits of the second
      * half), O(n log^2 n) steps instead of the counting rank's O(n^2)
      * compares (C4: 527 -> 511 ms) */
     int N = 1024;
     while (N / 2 >= n_all) N >>= 1;
-    for (int j = tid; j < N; j += nthr) {
-      const SKey k = skey_of(w, j, n_all); /* j >= n_all: (~0, ~0), sorts last */
-      key[j] = make_ulonglong2(k.k1, k.k2);
+    /* the network runs in registers: thread tid holds elements tid and
+     * tid + NT (N = 1024); exchanges between elements of one warp (j <= 16)
+     * are shuffles, between warps a shared-memory round (ping-pong between
+     * the key buffer and the not-yet-written sorted view: one barrier per
+     * cross-warp step, 10-14 instead of one per step, 45-55) */
+    constexpr int NT = 512; /* the branch is taken by the 512-thread team only */
+    ulonglong2 v[2];
+    for (int e = 0; e < 2; e++) {
+      const int i = tid + e * NT;
+      if (i < N) {
+        const SKey k = skey_of(w, i, n_all); /* i >= n_all: (~0, ~0), sorts last */
+        v[e] = make_ulonglong2(k.k1, k.k2);
+      }
     }
-    ec_team_barrier(W::NT);
     EC_QPROF(w, 0);
+    ulonglong2* bufs[2] = {key, reinterpret_cast<ulonglong2*>(w->srt)};
+    static_assert(sizeof(SortE) == sizeof(ulonglong2), "the sorted view doubles as a key buffer");
+    int flip = 0;
+    auto keep = [](ulonglong2& me, const ulonglong2& o, bool take_min) {
+      const bool o_less = o.x < me.x || (o.x == me.x && o.y < me.y);
+      if (take_min == o_less) me = o;
+    };
     for (int k = 2; k <= N; k <<= 1) {
       for (int jj = k >> 1; jj > 0; jj >>= 1) {
-        for (int i = tid; i < N; i += nthr) {
-          const int ixj = i ^ jj;
-          if (ixj > i) {
-            const ulonglong2 x = key[i], y = key[ixj];
-            const bool gt = x.x > y.x || (x.x == y.x && x.y > y.y);
-            if (gt == ((i & k) == 0)) {
-              key[i] = y;
-              key[ixj] = x;
+        if (jj >= NT) { /* k = N = 1024, j = 512: the thread's own two elements */
+          const ulonglong2 a0 = v[0], a1 = v[1];
+          keep(v[0], a1, true); /* element tid < tid + 512, ascending (k = N) */
+          keep(v[1], a0, false);
+        } else if (jj >= 32) {
+          ulonglong2* buf = bufs[flip];
+          flip ^= 1;
+          for (int e = 0; e < 2; e++) {
+            const int i = tid + e * NT;
+            if (i < N) buf[i] = v[e];
+          }
+          ec_team_barrier(NT);
+          for (int e = 0; e < 2; e++) {
+            const int i = tid + e * NT;
+            if (i < N) {
+              const int pj = i ^ jj;
+              keep(v[e], buf[pj], (i < pj) == ((i & k) == 0));
+            }
+          }
+        } else {
+          for (int e = 0; e < 2; e++) {
+            const int i = tid + e * NT;
+            if (e * NT < N) { /* warp-uniform */
+              ulonglong2 o;
+              o.x = __shfl_xor_sync(0xffffffffu, v[e].x, jj);
+              o.y = __shfl_xor_sync(0xffffffffu, v[e].y, jj);
+              keep(v[e], o, (i < (i ^ jj)) == ((i & k) == 0));
             }
           }
         }
-        ec_team_barrier(W::NT);
       }
     }
+    ec_team_barrier(NT); /* every cross-warp read is done before the final store */
+    for (int e = 0; e < 2; e++) {
+      const int i = tid + e * NT;
+      if (i < N) key[i] = v[e];
+    }
+    ec_team_barrier(NT);
     EC_QPROF(w, 1);
     for (int p = tid; p < n_all; p += nthr) {
       const ulonglong2 kp = key[p];
