@@ -178,6 +178,7 @@ static_assert(sizeof(AgentHot) == 128, "one 128-byte line per agent");
 /* one agent's event cursor (agent state in registers) */
 struct Cur {
   int a, inst, phase, prio, steps, n_turns, sa;
+  int slot; /* the agent's alive slot (fixed between the speculation and the apply) */
   double t, llm, issue, anchor, rem, done;
   long long ctx, dec, maxctx, turn0;
   /* turn records of the current and the next turn, prefetched with the
@@ -472,6 +473,20 @@ EC_DEV void clear_event(const GP& g, int a, int inst) {
 }
 
 EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.sl[g.H[a].slot].tp, tp); }
+
+/* the same three with the alive slot already known (no dependent load of
+ * H[a].slot): the apply has it from the speculation's record load */
+EC_DEV void set_event_at(const GP& g, int a, int j, int inst, int prio, double t, long long seq) {
+  g.H[a].next_t = t;
+  g.H[a].next_prio = prio;
+  g.H[a].next_seq = seq;
+  EC_STK_EV(&g.sl[j], ec_f32_down(t), slot_meta(inst, prio, a));
+}
+EC_DEV void clear_event_at(const GP& g, int a, int j, int inst) {
+  g.H[a].next_prio = 0;
+  EC_STK_EV(&g.sl[j], EC_INF_F32, slot_meta(inst, 0, a));
+}
+EC_DEV void set_tp_at(const GP& g, int j, double tp) { EC_STK_F64(&g.sl[j].tp, tp); }
 
 /* a fresh slot j for agent a: pending on instance `inst`, no throughput yet */
 EC_DEV void init_slot(const GP& g, int j, int inst, int a) {
@@ -908,6 +923,7 @@ EC_DEV void cur_load(const GP& g, Cur& c, int a) {
   c.a = a;
   c.inst = h.inst;
   c.phase = h.phase;
+  c.slot = h.slot;
   c.prio = h.next_prio;
   c.t = h.next_t;
   c.steps = h.steps;
@@ -2794,18 +2810,18 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
     g.H[a].rem = c.rem;
     g.H[a].done = c.done;
     if (c.prio > 0)
-      set_event(g, a, c.inst, c.prio, c.t, nseq);
+      set_event_at(g, a, c.slot, c.inst, c.prio, c.t, nseq);
     else
-      clear_event(g, a, c.inst);
+      clear_event_at(g, a, c.slot, c.inst);
     if (srank >= 0) {
       g.H[a].start_rank = srank;
       g.H[a].logpos = lpos;
     }
     if (c.phase == ASB_PHASE_DONE) {
-      set_tp(g, a, EC_NAN);
+      set_tp_at(g, c.slot, EC_NAN);
       g.ctime[a] = c.t;
     } else if (c.llm > 0.0) {
-      set_tp(g, a, (double)c.dec / c.llm);
+      set_tp_at(g, c.slot, (double)c.dec / c.llm);
     }
   }
 }
