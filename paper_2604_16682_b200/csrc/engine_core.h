@@ -643,6 +643,17 @@ EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos
 /* add agents whose next event changed during the epoch (re-timed or just
  * admitted) to the due candidates, once each (team; `cand` per lane) */
 template <class W, int DCAP>
+EC_DEV void add_candidate_at(W* w, const GP& g, int a, bool cand, int stamp, double t) {
+  /* add_candidates with the agent's dedup stamp and next event time known */
+  const bool add = cand && a >= 0 && stamp != w->cand_token && (w->incl ? t <= w->bound : t < w->bound);
+  if (add) {
+    const int pos = t_atomic_add_i(&w->n_cand, 1);
+    if (pos < DCAP) w->due[pos] = a;
+    g.dstamp[a] = w->cand_token;
+  }
+}
+
+template <class W, int DCAP>
 EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
   bool add = false;
   if (cand && a >= 0 && g.dstamp[a] != w->cand_token) {
@@ -918,8 +929,9 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
  * -------------------------------------------------------------------------- */
 
 
-EC_DEV void cur_load(const GP& g, Cur& c, int a) {
+EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr) {
   const AgentHot h = g.H[a]; /* one line, 128-bit loads */
+  if (next_seq) *next_seq = h.next_seq;
   c.a = a;
   c.inst = h.inst;
   c.phase = h.phase;
@@ -1349,12 +1361,21 @@ EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, lon
     bool valid = j < n_adm;
     int a = valid ? g.ring[(long long)(i - 1) * g.A + ring_idx(head0, j, g.A)] : -1;
     bool start = false;
-    double issue = 0.0;
+    double issue = 0.0, nb = 0.0, t_next = 0.0;
+    int slot = 0, steps = 0, stamp = 0;
+    long long turn0 = 0;
     if (valid) {
+      /* everything this agent's start reads, in one round of independent
+       * loads after the FIFO entry (no dependent reload of H[a] fields) */
       double pi = g.pissue[a];
+      nb = g.notbefore[a];
+      slot = g.H[a].slot;
+      steps = g.H[a].steps;
+      turn0 = g.aturn[a];
+      if (collect) stamp = g.dstamp[a];
       issue = ec_isnan(pi) ? now : pi;
       g.pissue[a] = EC_NAN;
-      start = !(now < g.notbefore[a]);
+      start = !(now < nb);
     }
     unsigned m = t_ballot(start);
     int sidx = started + ec_popc(m & t_lt_mask());
@@ -1362,21 +1383,23 @@ EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, lon
       g.H[a].issue = issue;
       if (!start) {
         g.H[a].phase = ASB_PHASE_WAITING_START;
-        set_event(g, a, i, EV_ISSUE, g.notbefore[a], seq0 + j);
+        t_next = nb;
+        set_event_at(g, a, slot, i, EV_ISSUE, nb, seq0 + j);
       } else {
-        double dur = svc_time(w, g, g.aturn[a] + g.H[a].steps, lvl, 0, thr);
+        double dur = svc_time(w, g, turn0 + steps, lvl, 0, thr);
+        t_next = now + dur;
         g.H[a].anchor = now;
         g.H[a].rem = 1.0;
-        g.H[a].done = now + dur;
+        g.H[a].done = t_next;
         g.H[a].phase = ASB_PHASE_RUNNING;
-        set_event(g, a, i, EV_COMPLETE, now + dur, seq0 + j);
+        set_event_at(g, a, slot, i, EV_COMPLETE, t_next, seq0 + j);
         g.H[a].start_rank = rank0 + sidx;
         g.H[a].logpos = log0 + sidx;
         g.log[(long long)(i - 1) * g.A + log0 + sidx] = a;
       }
     }
     started += ec_popc(m);
-    if (collect) add_candidates<W, DCAP>(w, g, a, valid);
+    if (collect) add_candidate_at<W, DCAP>(w, g, a, valid, stamp, t_next);
   }
   t_sync();
   EC_LANE0 {
@@ -2365,10 +2388,11 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   int order_err = 0;
   for (int d = tid; d < nd; d += nthr) {
     Cur c;
-    cur_load(g, c, w->due[d]);
+    long long seq0;
+    cur_load(g, c, w->due[d], &seq0);
     if (W::CC) w->ccache[d] = c;
     Rec* r = &w->rec[d];
-    r->seq = g.H[c.a].next_seq;
+    r->seq = seq0;
     if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
       /* a candidate whose event moved out of the window (re-timed) */
       r->flags = F_EMPTY;
