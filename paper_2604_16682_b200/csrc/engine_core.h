@@ -338,11 +338,11 @@ EC_DEV int ec_nm(const W* w) {
   return (W::FIXM || W::MX == 1) ? W::MX : w->sc.n_instances;
 }
 
-/* optional sort timing (-DASB_PROFILE -DASB_PROFILE_SORT): thread 0's
- * cycles per JOB_SORT step in prof[0..5] */
-#if defined(ASB_PROFILE_SORT)
-#define EC_QPROF_T0() long long qprof_t_ = ec_clock()
-#define EC_QPROF(w, k)                               \
+/* optional sub-step timing of one team job: thread 0's cycles per step in
+ * prof[0..5], for JOB_SORT (-DASB_PROFILE -DASB_PROFILE_SORT, EC_QPROF) or
+ * the speculation (-DASB_PROFILE -DASB_PROFILE_SPEC, EC_PPROF) */
+#define EC_STEPPROF_T0_ long long qprof_t_ = ec_clock()
+#define EC_STEPPROF_(w, k)                           \
   do {                                               \
     if (tid == 0) {                                  \
       const long long qn_ = ec_clock();              \
@@ -350,13 +350,22 @@ EC_DEV int ec_nm(const W* w) {
       qprof_t_ = qn_;                                \
     }                                                \
   } while (0)
+#define EC_STEPPROF_NONE_ \
+  do {                    \
+  } while (0)
+#if defined(ASB_PROFILE_SORT)
+#define EC_QPROF_T0() EC_STEPPROF_T0_
+#define EC_QPROF(w, k) EC_STEPPROF_(w, k)
 #else
-#define EC_QPROF_T0() \
-  do {                \
-  } while (0)
-#define EC_QPROF(w, k) \
-  do {                 \
-  } while (0)
+#define EC_QPROF_T0() EC_STEPPROF_NONE_
+#define EC_QPROF(w, k) EC_STEPPROF_NONE_
+#endif
+#if defined(ASB_PROFILE_SPEC)
+#define EC_PPROF_T0() EC_STEPPROF_T0_
+#define EC_PPROF(w, k) EC_STEPPROF_(w, k)
+#else
+#define EC_PPROF_T0() EC_STEPPROF_NONE_
+#define EC_PPROF(w, k) EC_STEPPROF_NONE_
 #endif
 
 /* optional phase timing (built with -DASB_PROFILE): cycles per engine phase
@@ -403,7 +412,7 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_PROF(w, k) \
   do {                \
   } while (0)
-#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT)
+#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC)
 #define EC_WPROF_START(w) \
   do {                    \
   } while (0)
@@ -2386,11 +2395,13 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   unsigned long long my_t = EC_INF_BITS;
   unsigned my_p = 0;
   int order_err = 0;
+  EC_PPROF_T0();
   for (int d = tid; d < nd; d += nthr) {
     Cur c;
     long long seq0;
     cur_load(g, c, w->due[d], &seq0);
     if (W::CC) w->ccache[d] = c;
+    EC_PPROF(w, 1); /* the record and turn loads */
     Rec* r = &w->rec[d];
     r->seq = seq0;
     if (!(c.prio > 0 && (incl ? c.t <= bound : c.t < bound))) {
@@ -2403,6 +2414,7 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
       continue;
     }
     if (!cur_step(w, g, c, *r, false)) order_err = 1;
+    EC_PPROF(w, 2); /* the first event */
     while (c.prio > 0 && (incl ? c.t <= bound : c.t < bound)) {
       const int slot = t_atomic_add_i(&w->tmp_i, 1) + nr0;
       if (slot >= W::RC) {
@@ -2421,12 +2433,14 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
       if (!cur_step(w, g, c, *r, false)) order_err = 1;
     }
   }
+  EC_PPROF(w, 3); /* the chain's continuations */
   if (order_err) w->j_order_err = 1;
   t_warp_min_key(my_t, my_p);
   if ((tid & 31) == 0) {
     w->j_hz_t[tid >> 5] = my_t;
     w->j_hz_p[tid >> 5] = my_p;
   }
+  EC_PPROF(w, 4); /* the warp's horizon key */
 }
 
 /* JOB_SORT (thread-level): rank sort of the records by (time, prio, seq) —
@@ -3073,7 +3087,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   EC_PROF(w, 2);
-#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT)
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC)
   EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
   t_sync();
 #endif

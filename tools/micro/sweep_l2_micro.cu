@@ -16,7 +16,11 @@ struct alignas(16) Slot {
 template <int CG>
 __device__ __forceinline__ void ld(const Slot* p, double& tp, float& nx, int& m) {
   unsigned long long lo, hi;
-  if (CG)
+  if (CG == 2) {
+    unsigned long long pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("ld.global.L2::cache_hint.v2.b64 {%0, %1}, [%2], %3;" : "=l"(lo), "=l"(hi) : "l"(p), "l"(pol));
+  } else if (CG)
     asm volatile("ld.global.cg.v2.b64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p));
   else
     asm volatile("ld.global.v2.b64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(p));
@@ -89,6 +93,8 @@ int main() {
   run("L2 U=2", sweep<2, 1>, 0);
   run("L2 U=4", sweep<4, 1>, 0);
   run("L2 U=8", sweep<8, 1>, 0);
+  run("L1/L2 evict_last U=2", sweep<2, 2>, 0);
+  run("HBM evict_last U=2", sweep<2, 2>, (long long)per_rep * 2);
   run("HBM U=2", sweep<2, 1>, (long long)per_rep * 2);
   run("HBM U=4", sweep<4, 1>, (long long)per_rep * 2);
   run("HBM U=8", sweep<8, 1>, (long long)per_rep * 2);
