@@ -433,7 +433,7 @@ def main():
         if ev0 is not None:
             ev0.record(stream)
         torch.ops.agentsim_b200.run_scenarios(db.scen, db.traces, db.tables, db.out_list, db.workspace,
-                                              batch.launch_instances, batch.total_agents, batch.total_ring)
+                                              batch.launch_instances, batch.total_agents, batch.total_ring, batch.max_levels)
         if ev1 is not None:
             ev1.record(stream)
         torch.ops.agentsim_b200.scenario_stats(db.scen, db.out_list, db.stats)
@@ -517,7 +517,7 @@ def main():
             scen, traces, tables = inp[0], inp[1:1 + nt], inp[1 + nt:1 + nt + ntab]
             stream.wait_event(copied[k % 2])
             torch.ops.agentsim_b200.run_scenarios(scen, traces, tables, db.out_list, db.workspace,
-                                                  batch.launch_instances, batch.total_agents, batch.total_ring)
+                                                  batch.launch_instances, batch.total_agents, batch.total_ring, batch.max_levels)
             torch.ops.agentsim_b200.scenario_stats(scen, db.out_list, db.stats)
             used[k % 2].record(stream)
             torch.ops.agentsim_b200.reduce_stats(db.stats, db.outputs["counters"], batch.n, db.red)

@@ -43,6 +43,10 @@ extern "C" {
 #endif
 
 #define ASB_ABI_VERSION 1
+/* engine limits: instance ids fit 7 bits of an alive slot's meta word;
+ * frequency tables are staged in shared memory per scenario */
+#define ASB_MAX_INSTANCES 127
+#define ASB_MAX_LEVELS 64
 
 typedef enum {
   ASB_OK = 0,
@@ -134,7 +138,7 @@ typedef struct AsbTracePool {
 /* Frequency tables (instance.py:24-112), 1-based level l at table_off[t] + l - 1. */
 typedef struct AsbTablePool {
   int32_t n_tables;
-  int32_t pad_;
+  int32_t max_levels;              /* host-side: the largest level count in the pool, 0 = at most 16 */
   const int64_t* table_off;        /* [n_tables+1] */
   const double* mhz;
   const double* prefill_rate;

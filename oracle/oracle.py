@@ -45,7 +45,8 @@ def _load(path: str, fn: str, extra: list):
 
 def _structs(batch, arrays):
     tp = _abi.make_pool(_abi.AsbTracePool, _np_ptr, batch.traces.arrays(), "n_traces", batch.traces.n_traces)
-    tb = _abi.make_pool(_abi.AsbTablePool, _np_ptr, batch.tables.arrays(), "n_tables", batch.tables.n_tables)
+    tb = _abi.make_pool(_abi.AsbTablePool, _np_ptr, batch.tables.arrays(), "n_tables", batch.tables.n_tables,
+                        max_levels=batch.max_levels)
     out = _abi.make_outputs(_np_ptr, arrays)
     return tp, tb, out
 

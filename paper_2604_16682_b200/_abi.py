@@ -132,7 +132,7 @@ class AsbTracePool(C.Structure):
 class AsbTablePool(C.Structure):
     _fields_ = [
         ("n_tables", C.c_int32),
-        ("pad_", C.c_int32),
+        ("max_levels", C.c_int32),  # host-side: the largest level count (0: at most 16)
         ("table_off", P),
         ("mhz", P),
         ("prefill_rate", P),
@@ -215,11 +215,13 @@ def make_outputs(ptr_of, arrays: dict) -> AsbOutputs:
     return out
 
 
-def make_pool(cls, ptr_of, arrays: dict, count_field: str, count: int):
+def make_pool(cls, ptr_of, arrays: dict, count_field: str, count: int, **scalars):
     pool = cls()
     setattr(pool, count_field, count)
-    for name, _ in cls._fields_:
-        if name in (count_field, "pad_"):
+    for name, value in scalars.items():
+        setattr(pool, name, value)
+    for name, ctype in cls._fields_:
+        if name in (count_field, "pad_") or name in scalars or ctype is not P:
             continue
         setattr(pool, name, ptr_of(arrays[name]))
     return pool

@@ -285,7 +285,7 @@ __global__ void ring_offsets_kernel(const AsbScenario* scen, int n_scen, const i
   }
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int LMAX>
 /* min blocks per SM: 4-warp teams 4 per SM; single-warp teams 16 per SM,
  * i.e. <= 128 registers, so that 14 of them fit next to their shared memory
  * (C3's 2,048 scenarios in one wave of 148 x 14) */
@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
    * helpers joining the slot sweeps, speculation, rank sort and apply */
-  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT, LMAX>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   W* w = reinterpret_cast<W*>(smem_raw);
   if (threadIdx.x >= 32) {
@@ -381,16 +381,16 @@ __global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
   ec_fork_begin(NT);
 }
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int NT>
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int LMAX = 16>
 int launch_engine(const AsbScenario* d_scen, int n_scen, const AsbTracePool& tp, const AsbTablePool& tb,
                   const AsbOutputs& out, const Workspace& ws, cudaStream_t st) {
-  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT>;
+  using W = asb::WS<MAXM, RCAP, DCAP, ACAP, NT, LMAX>;
   static_assert(RCAP >= DCAP + ACAP, "record buffer must hold every first record");
   static_assert(NT % 32 == 0 && NT >= 32 && (NT & (NT - 1)) == 0, "team = a power-of-two number of whole warps");
   /* 4 teams per SM need <= ~54 KB of shared memory each (228 KB per SM) */
   static_assert(NT > 128 || W::MX > 16 || sizeof(W) <= 54 * 1024, "small-team workspace must allow 4 CTAs per SM");
   const size_t smem = (sizeof(W) + 15) / 16 * 16;
-  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT>;
+  auto kern = asb_engine_kernel<MAXM, RCAP, DCAP, ACAP, NT, LMAX>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return ASB_ERR_LAUNCH;
   int dev = 0, sms = 0, per_sm = 0;
@@ -434,7 +434,8 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
                       void* d_workspace, size_t workspace_bytes, void* stream) {
   const bool fixed_m = max_instances < 0; /* -m: every scenario has exactly m instances */
   if (fixed_m) max_instances = -max_instances;
-  if (n_scen < 0 || max_instances < 1 || max_instances > 64) return ASB_ERR_ARG;
+  if (n_scen < 0 || max_instances < 1 || max_instances > ASB_MAX_INSTANCES) return ASB_ERR_ARG;
+  if (tables.max_levels < 0 || tables.max_levels > ASB_MAX_LEVELS) return ASB_ERR_ARG;
   if (out.timeseries && (!out.ts_off || !out.ts_count)) return ASB_ERR_ARG; /* rows need their offsets and counts */
   if (n_scen == 0) return ASB_OK;
   size_t need = carve(nullptr, n_scen, total_agents, total_ring_slots, nullptr);
@@ -469,6 +470,10 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
     big = !strcmp(force, "big");
     solo = !strcmp(force, "solo");
   }
+  /* more than 64 instances or more than 16 DVFS levels: the wide kernel
+   * (128 instance slots, 64 levels; ~2 teams per SM, correctness first) */
+  if (max_instances > 64 || tables.max_levels > 16)
+    return launch_engine<128, 192, 128, 64, 128, ASB_MAX_LEVELS>(d_scen, n_scen, traces, tables, out, ws, st);
   if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   /* single-instance scenarios (the DVFS sweep): a kernel whose instance
    * count is the constant 1, with the per-instance machinery folded away */

@@ -237,7 +237,7 @@ struct GP {
 enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
        JOB_EPOCH = 7, JOB_FINISH = 8, JOB_DEPS = 9 };
 
-template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR>
+template <int MAXM, int RCAP, int DCAP, int ACAP, int NTHR, int LMAX = 16>
 struct WS {
   static constexpr int NT = NTHR;          /* threads of the team (main warp + helpers) */
   static constexpr int NW = (NTHR + 31) / 32;
@@ -293,7 +293,7 @@ struct WS {
   int n_rec, n_due, n_arr, stop_kind, stop_rec, flag, tmp_i, n_dep;
   int due_ready, n_cand, cand_token, n_empty, cand_collect;
   int stamp_ctr; /* last due-list stamp handed out (dstamp de-duplication) */
-  double pr[16], dr[16], act[16], idle[16];
+  double pr[LMAX], dr[LMAX], act[LMAX], idle[LMAX]; /* the scenario's frequency table (levels 1..L) */
   Inst in[MX];
   unsigned long long tmin[MX];
   /* epoch scratch (per instance) */
@@ -1856,10 +1856,12 @@ EC_COLD4 void route_parallel(W* w, int n_dep, int stop_p) {
   t_sync();
 }
 
-/* snap_argmin for M up to 64: each lane folds its instances into one 32-bit
- * key, one warp reduction; -1 when a usage does not fit the key */
+/* snap_argmin for M > 32: each lane folds its instances into one 32-bit
+ * key (usage << IDB | id, IDB = 6 bits of instance id, 7 for the 128-wide
+ * kernel), one warp reduction; -1 when a usage does not fit the key */
 template <class W>
 EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* bu_out) {
+  constexpr int IDB = W::MX > 64 ? 7 : 6;
   const int M = ec_nm(w);
   unsigned key = 0xffffffffu;
   bool wide = false;
@@ -1867,15 +1869,15 @@ EC_COLD4 int snap_argmin_wide(const W* w, int k, bool all, int cur, long long* b
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
     const long long u = w->snap[k][i - 1];
     if (!(all || u > 0 || i == cur)) continue;
-    wide |= u < 0 || u >= (1ll << 26);
-    const unsigned kk = ((unsigned)u << 6) | (unsigned)(i - 1);
+    wide |= u < 0 || u >= (1ll << (32 - IDB));
+    const unsigned kk = ((unsigned)u << IDB) | (unsigned)(i - 1);
     key = kk < key ? kk : key;
   }
   if (t_ballot(wide)) return -1;
   const unsigned mn = t_redux_min_u32(key);
   if (mn == 0xffffffffu) return 0;
-  *bu_out = (long long)(mn >> 6);
-  return (int)(mn & 63u) + 1;
+  *bu_out = (long long)(mn >> IDB);
+  return (int)(mn & ((1u << IDB) - 1u)) + 1;
 }
 
 /* Team argmin of (usage, id) over the usage snapshot k (router.py:91,123,150):

@@ -397,7 +397,7 @@ class DeviceBatch:
         if b.n == 0:
             return
         torch.ops.agentsim_b200.run_scenarios(self.scen, self.traces, self.tables, self.out_list, self.workspace,
-                                              b.launch_instances, b.total_agents, b.total_ring)
+                                              b.launch_instances, b.total_agents, b.total_ring, b.max_levels)
         torch.ops.agentsim_b200.scenario_stats(self.scen, self.out_list, self.stats)
         torch.ops.agentsim_b200.reduce_stats(self.stats, self.outputs["counters"], b.n, self.red)
 

@@ -62,14 +62,16 @@ def run_scenarios(
     max_instances: int,
     total_agents: int,
     total_ring: int,
+    max_levels: int = 0,
 ) -> None:
-    """Run every scenario of the batch on the GPU (asb_run_scenarios)."""
+    """Run every scenario of the batch on the GPU (asb_run_scenarios).
+    ``max_levels``: the largest frequency table of the batch (0: at most 16)."""
     lib = _native.lib()
     n_scen = scen.numel() // _abi.SCENARIO_DTYPE.itemsize
     tp = _abi.make_pool(_abi.AsbTracePool, _ptr, dict(zip(_abi.TRACE_FIELDS, traces)), "n_traces",
                         traces[0].numel() - 1)
     tb = _abi.make_pool(_abi.AsbTablePool, _ptr, dict(zip(_abi.TABLE_FIELDS, tables)), "n_tables",
-                        tables[0].numel() - 1)
+                        tables[0].numel() - 1, max_levels=max_levels)
     out = _abi.make_outputs(_ptr, dict(zip(OUT_NAMES, outputs)))
     with _on(scen):
         rc = lib.asb_run_scenarios(_ptr(scen), n_scen, max_instances, tp, tb, out, total_agents, total_ring,

@@ -162,6 +162,8 @@ def epoch_count(sim_duration: float, epoch_length: float) -> int:
 
 
 MAX_AGENTS = 1 << 21  # agent ids live in 21 bits of the engine's alive-slot word (engine_core.h Slot)
+MAX_INSTANCES = 127   # instance ids live in 7 bits of it (ASB_MAX_INSTANCES)
+MAX_LEVELS = 64       # ASB_MAX_LEVELS: frequency tables staged in shared memory
 
 
 def scenario_record(config, trace_id: int, table_id: int) -> tuple:
@@ -171,10 +173,11 @@ def scenario_record(config, trace_id: int, table_id: int) -> tuple:
     rt = config.router
     table = inst.frequency_table
     fixed_level = table.index_of_mhz(ctl.fixed_level_mhz) if ctl.variant == "fixed" else 0
-    if config.instance_count > 64:
-        raise ConfigurationError("instance_count: the B200 engine supports at most 64 instances per scenario")
-    if table.num_levels > 16:
-        raise ConfigurationError("frequency_table: the B200 engine supports at most 16 levels")
+    if config.instance_count > MAX_INSTANCES:
+        raise ConfigurationError(
+            f"instance_count: the B200 engine supports at most {MAX_INSTANCES} instances per scenario")
+    if table.num_levels > MAX_LEVELS:
+        raise ConfigurationError(f"frequency_table: the B200 engine supports at most {MAX_LEVELS} levels")
     rec = np.zeros((), dtype=_abi.SCENARIO_DTYPE)
     rec["trace_id"] = trace_id
     rec["table_id"] = table_id
@@ -246,6 +249,7 @@ class Batch:
     total_ring: int
     max_instances: int
     min_instances: int = 0
+    max_levels: int = 0      # the largest frequency table (AsbTablePool.max_levels)
 
     @property
     def n(self) -> int:
@@ -285,4 +289,5 @@ def build_batch(scen: np.ndarray, traces: TracePool, tables: TablePool) -> Batch
         total_ring=int((m * a_cnt).sum()),
         max_instances=int(m.max()) if n else 1,
         min_instances=int(m.min()) if n else 1,
+        max_levels=int(np.diff(tables.table_off).max()) if tables.table_off.size > 1 else 0,
     )

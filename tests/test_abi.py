@@ -51,3 +51,27 @@ def test_launch_instances_declares_fixed_counts():
     assert prepare_batch([base, base]).launch_instances == -4
     assert prepare_batch([base, dataclasses.replace(base, instance_count=1)]).launch_instances == 4
     assert prepare_batch([dataclasses.replace(base, instance_count=1)]).launch_instances == -1
+
+
+def test_engine_limits():
+    """127 instances and 64 DVFS levels are the engine's limits
+    (ASB_MAX_INSTANCES / ASB_MAX_LEVELS); one more raises ConfigurationError
+    before any launch, like the reference's own validation errors."""
+    import dataclasses
+
+    import pytest
+
+    import paper_2604_16682_b200 as asb
+    from paper_2604_16682_b200.engine import prepare_batch
+
+    traces = asb.generate_workload(asb.WorkloadSpec(arrival_rate=0.2, duration=30.0, seed=1))
+    t64 = asb.default_frequency_table(mhz=tuple(600.0 + 10.0 * k for k in range(64)))
+    ok = asb.SimConfig(traces=traces, instance_count=127, sim_duration=40.0,
+                       instance=asb.InstanceConfig(frequency_table=t64))
+    b = prepare_batch([ok])
+    assert b.max_levels == 64 and b.launch_instances == -127
+    with pytest.raises(asb.ConfigurationError):
+        prepare_batch([dataclasses.replace(ok, instance_count=128)])
+    t65 = asb.default_frequency_table(mhz=tuple(600.0 + 10.0 * k for k in range(65)))
+    with pytest.raises(asb.ConfigurationError):
+        prepare_batch([dataclasses.replace(ok, instance=asb.InstanceConfig(frequency_table=t65))])

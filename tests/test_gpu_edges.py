@@ -93,3 +93,44 @@ def test_single_config_batches_take_the_fixed_kernels(cuda_device):
     for k in ("completion_time", "llm_time", "turns_completed", "final_instance", "migrations"):
         assert np.array_equal(got_alone[k][:n0], got_mixed[k][:n0], equal_nan=got_alone[k].dtype.kind == "f"), k
     assert np.array_equal(got_alone["counters"][:_abi.ASB_NCOUNTERS], got_mixed["counters"][:_abi.ASB_NCOUNTERS])
+
+
+def _wide_configs(seed):
+    """Up to 127 instances and up to 64 DVFS levels (the wide kernel), with
+    every controller variant and router policy."""
+    import random
+
+    rng = random.Random(seed)
+    out = []
+    for m, n_lv in ((100, 24), (127, 8), (70, 64), (3, 40)):
+        traces = asb.generate_workload(asb.WorkloadSpec(arrival_rate=rng.choice([2.0, 5.0]), duration=150.0,
+                                                        seed=rng.randrange(10_000)))
+        table = asb.default_frequency_table(mhz=tuple(600.0 + 20.0 * k for k in range(n_lv)))
+        var = rng.choice(["context_aware", "off", "fixed"])
+        ctl = asb.ControllerConfig(variant=var, slo_target=rng.choice([20.0, 50.0]),
+                                   fixed_level_mhz=table.levels[n_lv // 2].nominal_mhz if var == "fixed" else None)
+        out.append(asb.SimConfig(traces=traces, instance_count=m, sim_duration=200.0,
+                                 instance=asb.InstanceConfig(frequency_table=table,
+                                                             capacity_tokens=rng.choice([3000, 30_000])),
+                                 controller=ctl,
+                                 router=asb.RouterConfig(policy=rng.choice(["context_aware", "round_robin",
+                                                                            "least_loaded"]),
+                                                         reassign_interval=rng.choice([1, 3]))))
+    return out
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_wide_kernel_matches_oracle(cuda_device, seed):
+    """More than 64 instances / more than 16 levels: the 128-instance,
+    64-level kernel, bit-exact against the oracle, rows included."""
+    batch = prepare_batch(_wide_configs(seed))
+    assert batch.max_levels > 16 and batch.max_instances > 64
+    _check(batch)
+    dev = DeviceBatch(batch, device="cuda:0", decisions=True, turn_log=True, timeseries=True)
+    dev.run()
+    got, _ = dev.download()
+    want, _ = run_oracle(batch, timeseries=True)
+    assert np.array_equal(got["ts_count"], want["ts_count"])
+    for s in range(batch.n):
+        o, n = int(batch.ts_off[s]), int(want["ts_count"][s])
+        assert got["timeseries"][o: o + n].tobytes() == want["timeseries"][o: o + n].tobytes(), s
