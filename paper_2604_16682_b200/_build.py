@@ -65,7 +65,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
     target = {"walk": WPROF_LIB_PATH, "debug": DEBUG_LIB_PATH,
               "sweep": os.path.join(LIB_DIR, "libagentsim_b200_sprof.so"),
               "sort": os.path.join(LIB_DIR, "libagentsim_b200_qprof.so"),
-              "spec": os.path.join(LIB_DIR, "libagentsim_b200_pprof.so")}.get(profile) if isinstance(profile, str) else (
+              "spec": os.path.join(LIB_DIR, "libagentsim_b200_pprof.so"),
+              "epoch": os.path.join(LIB_DIR, "libagentsim_b200_eprof.so")}.get(profile) if isinstance(profile, str) else (
         PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
@@ -82,6 +83,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
             cmd.insert(1, "-DASB_PROFILE_SORT")
         if profile == "spec":
             cmd.insert(1, "-DASB_PROFILE_SPEC")
+        if profile == "epoch":
+            cmd.insert(1, "-DASB_PROFILE_EPOCH")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)

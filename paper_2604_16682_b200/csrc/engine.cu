@@ -79,6 +79,16 @@ EC_COLL_UNROLL
   }
   return v;
 }
+EC_COLL int t_scan_add_i(int v) {
+EC_COLL_UNROLL
+  for (int o = 1; o < 32; o <<= 1) {
+    int n = __shfl_up_sync(FULLMASK, v, o);
+    if (EC_LANE >= o) v += n;
+  }
+  return v;
+}
+EC_DEV int t_shfl_i(int v, int src) { return __shfl_sync(FULLMASK, v, src); }
+EC_DEV int t_redux_add_i(int v) { return (int)__reduce_add_sync(FULLMASK, (unsigned)v); }
 EC_COLL long long t_sum_ll(long long v) {
 EC_COLL_UNROLL
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);

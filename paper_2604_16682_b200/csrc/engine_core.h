@@ -360,6 +360,13 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_QPROF_T0() EC_STEPPROF_NONE_
 #define EC_QPROF(w, k) EC_STEPPROF_NONE_
 #endif
+#if defined(ASB_PROFILE_EPOCH)
+#define EC_EPROF_T0() EC_STEPPROF_T0_
+#define EC_EPROF(w, k) EC_STEPPROF_(w, k)
+#else
+#define EC_EPROF_T0() EC_STEPPROF_NONE_
+#define EC_EPROF(w, k) EC_STEPPROF_NONE_
+#endif
 #if defined(ASB_PROFILE_SPEC)
 #define EC_PPROF_T0() EC_STEPPROF_T0_
 #define EC_PPROF(w, k) EC_STEPPROF_(w, k)
@@ -412,7 +419,7 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_PROF(w, k) \
   do {                \
   } while (0)
-#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC)
+#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH)
 #define EC_WPROF_START(w) \
   do {                    \
   } while (0)
@@ -1511,6 +1518,9 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
     return;
   }
   const double now = w->now;
+  const int tid = EC_LANE; /* sub-step profile: lane 0 of the main warp */
+  (void)tid;
+  EC_EPROF_T0();
   /* (a) lane per instance: observe, level, boost, level-hook power */
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
@@ -1547,22 +1557,25 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
       w->ep_gcap = (ca ? sc.gamma : 1.0) * (double)sc.capacity;
     }
     t_sync();
+    EC_EPROF(w, 0); /* (a) and the pending scan */
     if (cnt) {
       EC_SPROF_CNT(w, 5);
       fork_job(w, JOB_ADMIT);
     }
+    EC_EPROF(w, 1); /* (b) the admission job */
   }
   /* (c) lane per instance: deferral, thrash sync, rate key, push counts;
    * exclusive scans over instances -> each instance's first push seq and
    * first start rank (the reference pushes / starts instance-major) */
   long long seq_base = w->seq, rank_base = w->start_ctr;
   int flips = 0;
-  long long extra_retimes = 0, all_retimes = 0;
+  int extra_retimes = 0, all_retimes = 0; /* per epoch: at most the running agents */
   int nwork = 0;
+  constexpr bool single = W::MX == 1; /* one instance: lane 0 holds everything, no scans */
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int r0 = 0; r0 < M; r0 += EC_TSIZE) {
     const int i = r0 + EC_LANE + 1;
-    long long pushes = 0, starts = 0;
+    int pushes = 0, starts = 0; /* per instance and epoch: at most its agents */
     bool flip = false, work = false;
     if (i <= M) {
       Inst& in = w->in[i - 1];
@@ -1588,21 +1601,35 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
       starts = w->ep_nstart[i - 1];
       work = pushes > 0;
     }
+    if (single) { /* lane 0 is instance 1 and the only lane whose values are used */
+      flips += flip ? 1 : 0;
+      if (i <= M) {
+        w->ep_seq[0] = seq_base;
+        w->ep_rank[0] = rank_base;
+      }
+      seq_base += pushes;
+      rank_base += starts;
+      if (work) w->ep_list[0] = 1;
+      nwork += ec_popc(t_ballot(work)); /* warp-uniform: the fork below is taken by the whole warp */
+      continue;
+    }
     flips += ec_popc(t_ballot(flip));
-    const long long incl = t_scan_add_ll(pushes);
-    const long long incs = t_scan_add_ll(starts);
+    const int incl = t_scan_add_i(pushes);
+    const int incs = t_scan_add_i(starts);
     if (i <= M) {
       w->ep_seq[i - 1] = seq_base + incl - pushes;
       w->ep_rank[i - 1] = rank_base + incs - starts;
     }
-    seq_base += t_bcast_ll(incl, EC_TSIZE - 1);
-    rank_base += t_bcast_ll(incs, EC_TSIZE - 1);
+    seq_base += t_shfl_i(incl, EC_TSIZE - 1);
+    rank_base += t_shfl_i(incs, EC_TSIZE - 1);
     const unsigned m = t_ballot(work);
     if (work) w->ep_list[nwork + ec_popc(m & t_lt_mask())] = i;
     nwork += ec_popc(m);
   }
-  extra_retimes = t_sum_ll(extra_retimes);
-  all_retimes = t_sum_ll(all_retimes);
+  if (!single) {
+    extra_retimes = t_redux_add_i(extra_retimes);
+    all_retimes = t_redux_add_i(all_retimes);
+  }
   t_sync();
   EC_LANE0 {
     w->seq = seq_base;
@@ -1614,9 +1641,11 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   t_sync();
   /* (d)+(e) re-time in-flight turns where the rate key changed, then start
    * the admitted turns — instances in parallel, one warp each (JOB_EPOCH) */
+  EC_EPROF(w, 2); /* (c) deferral, thrash sync, keys, push scans */
   if (nwork) {
     fork_job(w, JOB_EPOCH);
   }
+  EC_EPROF(w, 3); /* (d)+(e) the re-time / start job */
   /* (f) lane per instance: final power, decision rows */
   EC_ILOOP /* per-instance loop: rolled (instruction cache) */
   for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
@@ -1625,6 +1654,7 @@ EC_COLD3 void epoch_event(W* w, const GP& g, long long k) {
   }
   EC_LANE0 w->due_ready = w->n_cand <= DCAP;
   t_sync();
+  EC_EPROF(w, 4); /* (f) final power, decision rows */
   EC_PROF(w, 1);
 }
 
@@ -3089,7 +3119,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   EC_PROF(w, 2);
-#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC)
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH)
   EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
   t_sync();
 #endif

@@ -29,6 +29,9 @@ static inline unsigned t_match_any_i(int) { return 1u; }
 static inline unsigned t_redux_min_u32(unsigned v) { return v; }
 static inline long long t_bcast_ll(long long v, int) { return v; }
 static inline long long t_scan_add_ll(long long v) { return v; }
+static inline int t_scan_add_i(int v) { return v; }
+static inline int t_shfl_i(int v, int) { return v; }
+static inline int t_redux_add_i(int v) { return v; }
 static inline long long t_sum_ll(long long v) { return v; }
 static inline unsigned long long t_shfl_xor_ull(unsigned long long v, int) { return v; }
 static inline long long t_shfl_xor_ll(long long v, int) { return v; }

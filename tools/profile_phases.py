@@ -14,8 +14,9 @@ WALK = os.environ.get("ASB_PROFILE_WALK") == "1"
 SWEEP = os.environ.get("ASB_PROFILE_SWEEP") == "1"
 SORT = os.environ.get("ASB_PROFILE_SORT") == "1"
 SPEC = os.environ.get("ASB_PROFILE_SPEC") == "1"
+EPOCH = os.environ.get("ASB_PROFILE_EPOCH") == "1"
 os.environ["ASB_LIB"] = os.environ.get("ASB_PROF_LIB") or _build.build_cuda(
-    profile="walk" if WALK else ("sweep" if SWEEP else ("sort" if SORT else ("spec" if SPEC else True))))
+    profile="walk" if WALK else ("sweep" if SWEEP else ("sort" if SORT else ("spec" if SPEC else ("epoch" if EPOCH else True)))))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -29,6 +30,10 @@ if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
 if SORT:  # thread 0's cycles per JOB_SORT step
     PHASES = ("q0_keys", "q1_bitonic", "q2_rank_emit", "q3_barrier", "q4_tie_check", "q5_inst_lists")
+    WALK = True
+if EPOCH:  # the main warp's cycles per epoch-event step
+    PHASES = ("e0_levels_power_pending", "e1_admit_job", "e2_keys_scans", "e3_retime_start_job", "e4_final_power",
+              "e5_unused")
     WALK = True
 if SPEC:  # thread 0's cycles per JOB_SPEC step
     PHASES = ("p0_unused", "p1_record_loads", "p2_first_event", "p3_chain", "p4_horizon_key", "p5_unused")
