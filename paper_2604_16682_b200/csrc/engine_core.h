@@ -2467,7 +2467,8 @@ EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
   }
   EC_PPROF(w, 3); /* the chain's continuations */
   if (order_err) w->j_order_err = 1;
-  t_warp_min_key(my_t, my_p);
+  /* the warp's smallest dropped key; almost always none (no drops) */
+  if (t_ballot(my_t != EC_INF_BITS)) t_warp_min_key(my_t, my_p);
   if ((tid & 31) == 0) {
     w->j_hz_t[tid >> 5] = my_t;
     w->j_hz_p[tid >> 5] = my_p;
@@ -2682,14 +2683,14 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
         if (ij && before == 0) w->icnt[ij - 1] += __popc(peers);
         __syncwarp();
       }
-      long long run = 0;
+      int run = 0;
       EC_ILOOP /* per-instance loop: rolled (instruction cache) */
       for (int base = 0; base < M; base += 32) {
         const int i = base + lane;
-        const long long c = i < M ? w->icnt[i] : 0;
-        const long long inc = t_scan_add_ll(c);
-        if (i < M) w->ioff[i] = (int)(run + inc - c);
-        run += t_bcast_ll(inc, 31);
+        const int c = i < M ? w->icnt[i] : 0; /* record counts: 32-bit scans */
+        const int inc = t_scan_add_i(c);
+        if (i < M) w->ioff[i] = run + inc - c;
+        run += t_shfl_i(inc, 31);
       }
       if (lane == 0) w->ioff[M] = (int)run;
       __syncwarp();
@@ -2738,7 +2739,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
   }
   ec_team_barrier(W::NT);
   if (wid == 0) {
-    long long run = 0;
+    int run = 0;
     EC_ILOOP /* per-instance loop: rolled (instruction cache) */
     for (int base = 0; base < M; base += 32) {
       const int i = base + lane;
@@ -2749,9 +2750,9 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
           w->kcc[c][i] = (unsigned short)cnt;
           cnt += t;
         }
-      const long long inc = t_scan_add_ll(cnt);
-      if (i < M) w->ioff[i] = (int)(run + inc - cnt);
-      run += t_bcast_ll(inc, 31);
+      const int inc = t_scan_add_i(cnt);
+      if (i < M) w->ioff[i] = run + inc - cnt;
+      run += t_shfl_i(inc, 31);
     }
     if (lane == 0) w->ioff[M] = (int)run;
   }
