@@ -79,7 +79,7 @@ EC_COLL_UNROLL
   }
   return v;
 }
-EC_COLL int t_scan_add_i(int v) {
+EC_DEV int t_scan_add_i(int v) {
 EC_COLL_UNROLL
   for (int o = 1; o < 32; o <<= 1) {
     int n = __shfl_up_sync(FULLMASK, v, o);

@@ -2054,11 +2054,7 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
     }
     ndep += ec_popc(m);
   }
-  EC_ILOOP
-  for (int o = EC_TSIZE / 2; o > 0; o >>= 1) {
-    int oc = t_shfl_xor_i(cut, o);
-    cut = oc < cut ? oc : cut;
-  }
+  cut = (int)t_redux_min_u32((unsigned)cut); /* cut >= 0 */
   EC_LANE0 w->n_dep = ndep < W::DEP ? ndep : W::DEP;
   t_sync();
   EC_WPROF(w, 0);
