@@ -66,7 +66,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
               "sweep": os.path.join(LIB_DIR, "libagentsim_b200_sprof.so"),
               "sort": os.path.join(LIB_DIR, "libagentsim_b200_qprof.so"),
               "spec": os.path.join(LIB_DIR, "libagentsim_b200_pprof.so"),
-              "epoch": os.path.join(LIB_DIR, "libagentsim_b200_eprof.so")}.get(profile) if isinstance(profile, str) else (
+              "epoch": os.path.join(LIB_DIR, "libagentsim_b200_eprof.so"),
+              "apply": os.path.join(LIB_DIR, "libagentsim_b200_aprof.so")}.get(profile) if isinstance(profile, str) else (
         PROF_LIB_PATH if profile else LIB_PATH)
     if force or _stale(target, deps):
         os.makedirs(LIB_DIR, exist_ok=True)
@@ -85,6 +86,8 @@ def build_cuda(force: bool = False, verbose: bool = False, profile: bool | str =
             cmd.insert(1, "-DASB_PROFILE_SPEC")
         if profile == "epoch":
             cmd.insert(1, "-DASB_PROFILE_EPOCH")
+        if profile == "apply":
+            cmd.insert(1, "-DASB_PROFILE_APPLY")
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         _run(cmd)

@@ -360,6 +360,13 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_QPROF_T0() EC_STEPPROF_NONE_
 #define EC_QPROF(w, k) EC_STEPPROF_NONE_
 #endif
+#if defined(ASB_PROFILE_APPLY)
+#define EC_APROF_T0() EC_STEPPROF_T0_
+#define EC_APROF(w, k) EC_STEPPROF_(w, k)
+#else
+#define EC_APROF_T0() EC_STEPPROF_NONE_
+#define EC_APROF(w, k) EC_STEPPROF_NONE_
+#endif
 #if defined(ASB_PROFILE_EPOCH)
 #define EC_EPROF_T0() EC_STEPPROF_T0_
 #define EC_EPROF(w, k) EC_STEPPROF_(w, k)
@@ -419,7 +426,7 @@ EC_DEV int ec_nm(const W* w) {
 #define EC_PROF(w, k) \
   do {                \
   } while (0)
-#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH)
+#elif defined(ASB_PROFILE) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH) && !defined(ASB_PROFILE_APPLY)
 #define EC_WPROF_START(w) \
   do {                    \
   } while (0)
@@ -2844,6 +2851,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
 template <class W>
 EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
   const int nd = w->n_due;
+  EC_APROF_T0();
   for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
     Cur c; /* unchanged since the speculation loaded it */
@@ -2851,6 +2859,7 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
       c = w->ccache[d];
     else
       cur_load(g, c, w->due[d]);
+    EC_APROF(w, 0); /* the cursor */
     int ri = d;
     long long nseq = -1, srank = -1;
     int lpos = -1;
@@ -2864,6 +2873,7 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
       }
       ri = r.child;
     }
+    EC_APROF(w, 1); /* the committed records */
     const int a = c.a;
     g.H[a].ctx = c.ctx;
     g.H[a].dec = c.dec;
@@ -2890,7 +2900,9 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
     } else if (c.llm > 0.0) {
       set_tp_at(g, c.slot, (double)c.dec / c.llm);
     }
+    EC_APROF(w, 2); /* the write-back */
   }
+  EC_APROF(w, 3); /* the loop's exit */
 }
 
 /* JOB_INIT (thread-level): per-agent state of a fresh scenario (engine.py:251-276) */
@@ -3116,7 +3128,7 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   }
   /* ---- 4. rank sort + sorted SoA view */
   EC_PROF(w, 2);
-#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH)
+#if defined(ASB_PROFILE) && !defined(ASB_PROFILE_WALK) && !defined(ASB_PROFILE_SWEEP) && !defined(ASB_PROFILE_SORT) && !defined(ASB_PROFILE_SPEC) && !defined(ASB_PROFILE_EPOCH) && !defined(ASB_PROFILE_APPLY)
   EC_LANE0 w->ctr[ASB_CTR_RETIMES] += w->n_rec; /* profile builds: sum of batch sizes */
   t_sync();
 #endif
@@ -3129,7 +3141,13 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
   EC_DBG(5, w->stop_kind);
   EC_PROF(w, 4);
   /* ---- 6. apply committed chain prefixes */
-  fork_job(w, JOB_APPLY);
+  {
+    const int tid = EC_LANE; /* sub-step profile: lane 0 of the main warp */
+    (void)tid;
+    EC_APROF_T0();
+    fork_job(w, JOB_APPLY);
+    EC_APROF(w, 4); /* the apply fork-join, as the main warp sees it */
+  }
   EC_DBG(6, w->ctr[ASB_CTR_BATCHES]);
   EC_LANE0 w->ctr[ASB_CTR_BATCHES]++;
   /* ---- 7. coupling / overflow follow-ups */
@@ -3144,7 +3162,13 @@ EC_COLD3 int batch(W* w, const GP& g, double win_end) {
       w->cand_collect = keep;
     }
     t_sync();
-    exec_serial(w, g, w->stop_r); /* smem record: no local-memory copy */
+    {
+      const int tid = EC_LANE;
+      (void)tid;
+      EC_APROF_T0();
+      exec_serial(w, g, w->stop_r); /* smem record: no local-memory copy */
+      EC_APROF(w, 5); /* the coupling event, serially */
+    }
     EC_LANE0 {
       w->cand_collect = 0;
       w->due_ready = keep && w->n_cand <= DCAP;

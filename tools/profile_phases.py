@@ -15,8 +15,9 @@ SWEEP = os.environ.get("ASB_PROFILE_SWEEP") == "1"
 SORT = os.environ.get("ASB_PROFILE_SORT") == "1"
 SPEC = os.environ.get("ASB_PROFILE_SPEC") == "1"
 EPOCH = os.environ.get("ASB_PROFILE_EPOCH") == "1"
+APPLY = os.environ.get("ASB_PROFILE_APPLY") == "1"
 os.environ["ASB_LIB"] = os.environ.get("ASB_PROF_LIB") or _build.build_cuda(
-    profile="walk" if WALK else ("sweep" if SWEEP else ("sort" if SORT else ("spec" if SPEC else ("epoch" if EPOCH else True)))))
+    profile="walk" if WALK else ("sweep" if SWEEP else ("sort" if SORT else ("spec" if SPEC else ("epoch" if EPOCH else ("apply" if APPLY else True))))))
 
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
@@ -30,6 +31,9 @@ if WALK:
     PHASES = ("w0_deplist", "w1_replay", "w2_checks", "w3_writeback", "w4_scans", "w5_arrivals")
 if SORT:  # thread 0's cycles per JOB_SORT step
     PHASES = ("q0_keys", "q1_bitonic", "q2_rank_emit", "q3_barrier", "q4_tie_check", "q5_inst_lists")
+    WALK = True
+if APPLY:  # cycles per apply step (thread 0 inside the job; lane 0 of the main warp for 4, 5)
+    PHASES = ("a0_cursor", "a1_records", "a2_writeback", "a3_loop_exit", "a4_apply_forkjoin", "a5_coupling_serial")
     WALK = True
 if EPOCH:  # the main warp's cycles per epoch-event step
     PHASES = ("e0_levels_power_pending", "e1_admit_job", "e2_keys_scans", "e3_retime_start_job", "e4_final_power",
