@@ -619,6 +619,26 @@ EC_COLD4 int argmin_usage(const W* w, int cand_mode, int current) {
   return best;
 }
 
+/* argmin_usage by the whole warp: a lane per instance, one 32-bit REDUX of
+ * usage << 7 | id; *ok = false (result unused) when a usage does not fit */
+template <class W>
+EC_COLD4 int argmin_usage_team(const W* w, int cand_mode, int current, bool* ok) {
+  const int M = ec_nm(w);
+  unsigned key = 0xffffffffu;
+  bool wide = false;
+  EC_ILOOP /* per-instance loop: rolled (instruction cache) */
+  for (int i = EC_LANE + 1; i <= M; i += EC_TSIZE) {
+    const long long u = w->in[i - 1].usage;
+    if (cand_mode == 1 && !(u > 0 || i == current)) continue;
+    wide |= u < 0 || u >= (1ll << 25);
+    const unsigned kk = ((unsigned)u << 7) | (unsigned)(i - 1);
+    key = kk < key ? kk : key;
+  }
+  *ok = !t_ballot(wide);
+  const unsigned mn = t_redux_min_u32(key);
+  return mn == 0xffffffffu ? 0 : (int)(mn & 127u) + 1;
+}
+
 /* maybe_reassign decision once the counter reached the interval (router.py:110-128) */
 template <class W>
 EC_COLD4 int reassign_target(const W* w, int current) {
@@ -880,6 +900,17 @@ EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
 template <class W>
 EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
   int source = g.H[a].inst;
+  /* the reassignment check's argmin over the instances by the whole warp
+   * (many instances: a serial loop on lane 0 would dominate the event) */
+  int team_target = 0;
+  bool team_ok = false;
+  if (W::MX > 1 && w->sc.policy == ASB_POLICY_CONTEXT_AWARE && g.H[a].sa + 1 >= w->sc.reassign_interval) {
+    const int best = argmin_usage_team(w, w->sc.include_idle ? 0 : 1, source, &team_ok);
+    team_target = best && best != source &&
+                          (double)w->in[source - 1].usage >= w->sc.imbalance_ratio * (double)w->in[best - 1].usage
+                      ? best
+                      : 0;
+  }
   t_sync(); /* every lane has read the source before lane 0 migrates the agent */
   EC_LANE0 {
     int target = 0;
@@ -887,7 +918,7 @@ EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
     if (w->sc.policy == ASB_POLICY_CONTEXT_AWARE) {
       int sa = g.H[a].sa + 1;
       if (sa >= w->sc.reassign_interval) {
-        target = reassign_target(w, source);
+        target = team_ok ? team_target : reassign_target(w, source);
         if (target || !w->sc.reset_only_on_reassign) sa = 0;
       }
       g.H[a].sa = sa;
@@ -952,7 +983,7 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
  * -------------------------------------------------------------------------- */
 
 
-EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr) {
+EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr, bool with_turns = true) {
   const AgentHot h = g.H[a]; /* one line, 128-bit loads */
   if (next_seq) *next_seq = h.next_seq;
   c.a = a;
@@ -973,6 +1004,10 @@ EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr) 
   c.ctx = h.ctx;
   c.dec = h.dec;
   c.maxctx = h.maxctx;
+  if (!with_turns) { /* the apply replays records: no turn data needed */
+    c.pf_step = -2;
+    return;
+  }
   /* the turn data the next two events read (complete: turn k; issue: k or k+1) */
   const long long k = c.turn0 + c.steps;
   const bool ok0 = c.steps < c.n_turns, ok1 = c.steps + 1 < c.n_turns;
@@ -2858,7 +2893,7 @@ EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
     if (W::CC)
       c = w->ccache[d];
     else
-      cur_load(g, c, w->due[d]);
+      cur_load(g, c, w->due[d], nullptr, false);
     EC_APROF(w, 0); /* the cursor */
     int ri = d;
     long long nseq = -1, srank = -1;
