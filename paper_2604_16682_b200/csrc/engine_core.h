@@ -1354,7 +1354,13 @@ EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nul
     int a = valid ? ring[ring_idx(head, j, g.A)] : -1;
     long long c = valid ? g.H[a].ctx : 0;
     const double nb = valid ? g.notbefore[a] : 0.0;
-    long long incl = t_scan_add_ll(c);
+    /* prefix sums of the pending contexts: 32-bit when every one is below
+     * 2^26 (32 of them cannot overflow), else 64-bit */
+    long long incl;
+    if (!t_ballot(c >= (1ll << 26)))
+      incl = t_scan_add_i((int)c);
+    else
+      incl = t_scan_add_ll(c);
     long long excl = incl - c;
     bool ok = valid && (double)(usage + excl) < gcap;
     unsigned m = t_ballot(ok);
