@@ -1202,6 +1202,12 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   const int incl = w->j_incl, token = w->j_token;
   const int n = w->n_alive;
   int dead = 0, counted = 0;
+  /* the scenario's pointers in registers: read through the shared GP they
+   * would be reloaded after every shared-memory store of the loop */
+  const Slot* const sl = g.sl;
+  int* const dstamp = g.dstamp;
+  const AgentHot* const hot = g.H;
+  const long long* const aturn = g.aturn;
 #if defined(ASB_PROFILE_SWEEP)
   const long long js_t0 = ec_clock();
 #endif
@@ -1214,7 +1220,7 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
   for (int u = 0; u < U; u++) {
     const int j = u * nthr + tid;
     mt[u] = -1;
-    if (j < n) EC_LDK_SLOT(&g.sl[j], tp[u], nx[u], mt[u]);
+    if (j < n) EC_LDK_SLOT(&sl[j], tp[u], nx[u], mt[u]);
   }
   for (int base = 0; base < n; base += nthr * U) {
     const int nb = base + nthr * U;
@@ -1222,7 +1228,7 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
     for (int u = 0; u < U; u++) {
       const int j = nb + u * nthr + tid;
       mt2[u] = -1;
-      if (j < n) EC_LDK_SLOT(&g.sl[j], tp2[u], nx2[u], mt2[u]);
+      if (j < n) EC_LDK_SLOT(&sl[j], tp2[u], nx2[u], mt2[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
@@ -1234,13 +1240,13 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
           const int a = sm_agent(mt[u]);
           const int pos = t_atomic_add_i(&w->j_total, 1);
           if (pos < W::DC) w->due[pos] = a;
-          g.dstamp[a] = token;
+          dstamp[a] = token;
           /* the speculation reads this agent's record and turn offsets after
            * the epoch: start bringing them into L2 now (not on the 16-warp
            * team, whose sweeps collect hundreds: C4 +4% with it) */
           if (W::NT < 512) {
-            EC_PREFETCH_L2(&g.H[a]);
-            EC_PREFETCH_L2(&g.aturn[a]);
+            EC_PREFETCH_L2(&hot[a]);
+            EC_PREFETCH_L2(&aturn[a]);
           }
         }
       }
@@ -1251,14 +1257,8 @@ EC_COLD1 void job_sweep(W* w, const GP& g, int tid, int nthr) {
       const unsigned long long b = ec_bits(tp[u]);
       if (b > EC_INF_BITS)
         dead++;
-#if defined(ASB_EXP_SWEEP_NOMIN)
-      else if (b == 1) w->tmin[0] = b; /* experiment: no min */
-#elif defined(ASB_EXP_SWEEP_RACY)
-      else if (b < w->tmin[sm_inst(mt[u]) - 1]) w->tmin[sm_inst(mt[u]) - 1] = b; /* experiment: racy */
-#else
       else if (b < w->tmin[sm_inst(mt[u]) - 1])
         t_atomic_min_ull(&w->tmin[sm_inst(mt[u]) - 1], b);
-#endif
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
