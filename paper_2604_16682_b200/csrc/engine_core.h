@@ -234,6 +234,36 @@ struct GP {
   int A, M, L;
 };
 
+/* the scenario pointers a team job's loop reads, copied out of the shared
+ * GP once: read through the GP reference they are reloaded after every
+ * shared-memory store the loop makes (the compiler cannot rule out that the
+ * store changed them).  Passed by value to the inline cursor helpers. */
+struct GV {
+  AgentHot* H;
+  Slot* sl;
+  const long long* aturn;
+  const int* prefill;
+  const int* decode;
+  const double* tool;
+  double* ctime;
+  double *turn_issue, *turn_done;
+  long long turn_base;
+};
+EC_DEV GV gview(const GP& g) {
+  GV v;
+  v.H = g.H;
+  v.sl = g.sl;
+  v.aturn = g.aturn;
+  v.prefill = g.prefill;
+  v.decode = g.decode;
+  v.tool = g.tool;
+  v.ctime = g.ctime;
+  v.turn_issue = g.turn_issue;
+  v.turn_done = g.turn_done;
+  v.turn_base = g.turn_base;
+  return v;
+}
+
 enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
        JOB_EPOCH = 7, JOB_FINISH = 8, JOB_DEPS = 9 };
 
@@ -499,17 +529,20 @@ EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.sl[g.H[a].slot
 
 /* the same three with the alive slot already known (no dependent load of
  * H[a].slot): the apply has it from the speculation's record load */
-EC_DEV void set_event_at(const GP& g, int a, int j, int inst, int prio, double t, long long seq) {
+template <class G>
+EC_DEV void set_event_at(const G& g, int a, int j, int inst, int prio, double t, long long seq) {
   g.H[a].next_t = t;
   g.H[a].next_prio = prio;
   g.H[a].next_seq = seq;
   EC_STK_EV(&g.sl[j], ec_f32_down(t), slot_meta(inst, prio, a));
 }
-EC_DEV void clear_event_at(const GP& g, int a, int j, int inst) {
+template <class G>
+EC_DEV void clear_event_at(const G& g, int a, int j, int inst) {
   g.H[a].next_prio = 0;
   EC_STK_EV(&g.sl[j], EC_INF_F32, slot_meta(inst, 0, a));
 }
-EC_DEV void set_tp_at(const GP& g, int j, double tp) { EC_STK_F64(&g.sl[j].tp, tp); }
+template <class G>
+EC_DEV void set_tp_at(const G& g, int j, double tp) { EC_STK_F64(&g.sl[j].tp, tp); }
 
 /* a fresh slot j for agent a: pending on instance `inst`, no throughput yet */
 EC_DEV void init_slot(const GP& g, int j, int inst, int a) {
@@ -983,7 +1016,8 @@ EC_COLD2 void exec_serial(W* w, const GP& g, const Rec& r) {
  * -------------------------------------------------------------------------- */
 
 
-EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr, bool with_turns = true) {
+template <class G>
+EC_DEV void cur_load(const G& g, Cur& c, int a, long long* next_seq = nullptr, bool with_turns = true) {
   const AgentHot h = g.H[a]; /* one line, 128-bit loads */
   if (next_seq) *next_seq = h.next_seq;
   c.a = a;
@@ -1020,7 +1054,8 @@ EC_DEV void cur_load(const GP& g, Cur& c, int a, long long* next_seq = nullptr, 
 }
 
 /* prefill / decode tokens of the cursor's current turn (prefetched when possible) */
-EC_DEV void cur_turn_pd(const GP& g, const Cur& c, int& p, int& d) {
+template <class G>
+EC_DEV void cur_turn_pd(const G& g, const Cur& c, int& p, int& d) {
   if (c.steps == c.pf_step) {
     p = c.pf_p0;
     d = c.pf_d0;
@@ -1047,8 +1082,8 @@ EC_COLD4 double svc_time_pd(const W* w, int p, int d, int level, int concurrent,
 /* Advance the cursor over its next event, filling record r.  Mirrors the
  * agent-local part of _on_complete / _on_tool / _on_delayed_start. Returns
  * false on an event-order violation (child scheduled at or before parent). */
-template <class W>
-EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
+template <class W, class G>
+EC_DEV bool cur_step(const W* w, const G& g, Cur& c, Rec& r, bool apply) {
   r.t = c.t;
   r.prio = (short)c.prio;
   r.agent = c.a;
@@ -1114,8 +1149,8 @@ EC_DEV bool cur_step(const W* w, const GP& g, Cur& c, Rec& r, bool apply) {
 
 /* Re-apply a committed record to the cursor from the record alone (no trace
  * reads): the write-back half of cur_step. */
-template <class W>
-EC_DEV void cur_apply(const W* w, const GP& g, Cur& c, const Rec& r) {
+template <class W, class G>
+EC_DEV void cur_apply(const W* w, const G& g, Cur& c, const Rec& r) {
   if (r.prio == EV_COMPLETE) {
     if (g.turn_issue) {
       const long long turn = c.turn0 + c.steps;
@@ -2463,7 +2498,8 @@ EC_COLD3 bool walk_parallel(W* w, const GP& g, const int n) {
  * chains inside the window; continuation records are allocated atomically;
  * the smallest dropped key becomes the batch horizon. */
 template <class W>
-EC_COLD1 void job_spec(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_spec(W* w, const GP& gp, int tid, int nthr) {
+  const GV g = gview(gp);
   const double bound = w->j_bound;
   const int incl = w->j_incl;
   const int nd = w->n_due;
@@ -2890,7 +2926,8 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
 /* JOB_APPLY (thread-level): write back every due agent's committed chain
  * prefix (records carry everything, no trace reads) and its alive slot. */
 template <class W>
-EC_COLD1 void job_apply(W* w, const GP& g, int tid, int nthr) {
+EC_COLD1 void job_apply(W* w, const GP& gp, int tid, int nthr) {
+  const GV g = gview(gp);
   const int nd = w->n_due;
   EC_APROF_T0();
   for (int d = tid; d < nd; d += nthr) {
