@@ -248,6 +248,9 @@ struct GV {
   double* ctime;
   double *turn_issue, *turn_done;
   long long turn_base;
+  int *ring, *log, *dstamp, *rank;
+  double *pissue, *notbefore;
+  int A;
 };
 EC_DEV GV gview(const GP& g) {
   GV v;
@@ -261,8 +264,31 @@ EC_DEV GV gview(const GP& g) {
   v.turn_issue = g.turn_issue;
   v.turn_done = g.turn_done;
   v.turn_base = g.turn_base;
+  v.ring = g.ring;
+  v.log = g.log;
+  v.dstamp = g.dstamp;
+  v.rank = g.rank;
+  v.pissue = g.pissue;
+  v.notbefore = g.notbefore;
+  v.A = g.A;
   return v;
 }
+
+/* GV for the multi-warp teams; the single-warp teams keep reading through
+ * the shared GP (the view's registers cost them more than the reloads) */
+template <bool VIEW>
+struct GPick {
+  using T = GV;
+};
+template <>
+struct GPick<false> {
+  using T = const GP&;
+};
+template <bool VIEW>
+struct GTag {};
+EC_DEV GV gpick(const GP& g, GTag<true>) { return gview(g); }
+EC_DEV const GP& gpick(const GP& g, GTag<false>) { return g; }
+#define EC_GVIEW(W_, gp_) typename GPick<(W_::NT > 32)>::T g = gpick(gp_, GTag<(W_::NT > 32)>())
 
 enum { JOB_EXIT = 0, JOB_INIT = 1, JOB_SWEEP = 2, JOB_SPEC = 3, JOB_SORT = 4, JOB_APPLY = 5, JOB_ADMIT = 6,
        JOB_EPOCH = 7, JOB_FINISH = 8, JOB_DEPS = 9 };
@@ -512,7 +538,8 @@ EC_DEV bool below_horizon(unsigned long long tb, unsigned pr, long long seq, uns
 }
 
 /* next-event bookkeeping: per-agent copy + the alive-slot copy the sweeps read */
-EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long long seq) {
+template <class G>
+EC_DEV void set_event(const G& g, int a, int inst, int prio, double t, long long seq) {
   g.H[a].next_t = t;
   g.H[a].next_prio = prio;
   g.H[a].next_seq = seq;
@@ -520,12 +547,14 @@ EC_DEV void set_event(const GP& g, int a, int inst, int prio, double t, long lon
   EC_STK_EV(&g.sl[j], ec_f32_down(t), slot_meta(inst, prio, a));
 }
 
-EC_DEV void clear_event(const GP& g, int a, int inst) {
+template <class G>
+EC_DEV void clear_event(const G& g, int a, int inst) {
   g.H[a].next_prio = 0;
   EC_STK_EV(&g.sl[g.H[a].slot], EC_INF_F32, slot_meta(inst, 0, a));
 }
 
-EC_DEV void set_tp(const GP& g, int a, double tp) { EC_STK_F64(&g.sl[g.H[a].slot].tp, tp); }
+template <class G>
+EC_DEV void set_tp(const G& g, int a, double tp) { EC_STK_F64(&g.sl[g.H[a].slot].tp, tp); }
 
 /* the same three with the alive slot already known (no dependent load of
  * H[a].slot): the apply has it from the speculation's record load */
@@ -545,7 +574,8 @@ template <class G>
 EC_DEV void set_tp_at(const G& g, int j, double tp) { EC_STK_F64(&g.sl[j].tp, tp); }
 
 /* a fresh slot j for agent a: pending on instance `inst`, no throughput yet */
-EC_DEV void init_slot(const GP& g, int j, int inst, int a) {
+template <class G>
+EC_DEV void init_slot(const G& g, int j, int inst, int a) {
   EC_STK_F64(&g.sl[j].tp, EC_INF);
   EC_STK_EV(&g.sl[j], 0.0f, slot_meta(inst, 0, a));
 }
@@ -718,8 +748,8 @@ EC_COLD4 void commit_arrival(W* w, const GP& g, int a, int target, int order_pos
 
 /* add agents whose next event changed during the epoch (re-timed or just
  * admitted) to the due candidates, once each (team; `cand` per lane) */
-template <class W, int DCAP>
-EC_DEV void add_candidate_at(W* w, const GP& g, int a, bool cand, int stamp, double t) {
+template <class W, int DCAP, class G>
+EC_DEV void add_candidate_at(W* w, const G& g, int a, bool cand, int stamp, double t) {
   /* add_candidates with the agent's dedup stamp and next event time known */
   const bool add = cand && a >= 0 && stamp != w->cand_token && (w->incl ? t <= w->bound : t < w->bound);
   if (add) {
@@ -729,8 +759,8 @@ EC_DEV void add_candidate_at(W* w, const GP& g, int a, bool cand, int stamp, dou
   }
 }
 
-template <class W, int DCAP>
-EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
+template <class W, int DCAP, class G>
+EC_DEV void add_candidates(W* w, const G& g, int a, bool cand) {
   bool add = false;
   if (cand && a >= 0 && g.dstamp[a] != w->cand_token) {
     const double t = g.H[a].next_t;
@@ -752,8 +782,9 @@ EC_DEV void add_candidates(W* w, const GP& g, int a, bool cand) {
  * (engine.py:355-372) with push sequence numbers seq0, seq0+1, ...  Returns
  * the number of live entries (== running turns).  (team) */
 template <class W, int DCAP = 0>
-EC_COLD2 int log_pass(W* w, const GP& g, int i, int retime, long long seq0, double now, bool collect = false,
+EC_COLD2 int log_pass(W* w, const GP& gp, int i, int retime, long long seq0, double now, bool collect = false,
                     bool count = true) {
+  EC_GVIEW(W, gp);
   Inst& in = w->in[i - 1];
   const int len = in.log_len;
   int* lg = g.log + (long long)(i - 1) * g.A;
@@ -782,7 +813,7 @@ EC_COLD2 int log_pass(W* w, const GP& g, int i, int retime, long long seq0, doub
           rem *= (x > 0.0 ? x : 0.0);
         }
         long long turn = g.aturn[a] + g.H[a].steps;
-        double full = svc_time(w, g, turn, level, running, thr);
+        double full = svc_time(w, gp, turn, level, running, thr);
         done = now + rem * full;
         g.H[a].anchor = now;
         g.H[a].rem = rem;
@@ -878,7 +909,8 @@ EC_COLD2 void start_turn_serial(W* w, const GP& g, int i, int a, double issue) {
 
 /* _on_complete, engine.py:509-535 */
 template <class W>
-EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
+EC_COLD2 void complete_serial(W* w, const GP& gp, int a) {
+  EC_GVIEW(W, gp);
   int i = g.H[a].inst;
   EC_LANE0 {
     Inst& in = w->in[i - 1];
@@ -921,17 +953,18 @@ EC_COLD2 void complete_serial(W* w, const GP& g, int a) {
     count_flip(w, i, now);
   }
   t_sync();
-  cond_changed(w, g, i);
+  cond_changed(w, gp, i);
   EC_LANE0 {
     update_power(w, i, w->now);
-    ts_mark(w, g, i);
+    ts_mark(w, gp, i);
   }
   t_sync();
 }
 
 /* _on_tool, engine.py:537-561 */
 template <class W>
-EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
+EC_COLD2 void tool_serial(W* w, const GP& gp, int a) {
+  EC_GVIEW(W, gp);
   int source = g.H[a].inst;
   /* the reassignment check's argmin over the instances by the whole warp
    * (many instances: a serial loop on lane 0 would dominate the event) */
@@ -978,16 +1011,16 @@ EC_COLD2 void tool_serial(W* w, const GP& g, int a) {
   }
   t_sync();
   if (!w->flag) {
-    start_turn_serial(w, g, source, a, w->now);
-    EC_LANE0 ts_mark(w, g, source);
+    start_turn_serial(w, gp, source, a, w->now);
+    EC_LANE0 ts_mark(w, gp, source);
     t_sync();
     return;
   }
-  cond_changed(w, g, source);
+  cond_changed(w, gp, source);
   EC_LANE0 {
     update_power(w, source, w->now);
-    ts_mark(w, g, source);
-    ts_mark(w, g, g.H[a].inst); /* the target, engine.py:560-561 */
+    ts_mark(w, gp, source);
+    ts_mark(w, gp, g.H[a].inst); /* the target, engine.py:560-561 */
   }
   t_sync();
 }
@@ -1371,7 +1404,8 @@ EC_COLD3 void tick_sweep(W* w, const GP& g, bool collect, double bound, int incl
 
 /* β/γ FIFO admission as a prefix scan (controller.py:112-130); returns count (team) */
 template <class W>
-EC_COLD3 int admission(W* w, const GP& g, int i, double gcap, int* n_start = nullptr) {
+EC_COLD3 int admission(W* w, const GP& gp, int i, double gcap, int* n_start = nullptr) {
+  EC_GVIEW(W, gp);
   Inst& in = w->in[i - 1];
   const int len = in.fifo_len, head = in.fifo_head;
   const int* ring = g.ring + (long long)(i - 1) * g.A;
@@ -1448,10 +1482,11 @@ EC_COLD4 int choose_level(const W* w, int i, int* boosted) {
 /* start the admitted agents' turns of instance i (engine.py:458-473), no
  * interference: durations are independent, pushes numbered from seq0 (team) */
 template <class W, int DCAP>
-EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, long long seq0, long long rank0,
+EC_COLD3 void start_admitted(W* w, const GP& gp, int i, int head0, int n_adm, long long seq0, long long rank0,
                            bool collect) {
+  EC_GVIEW(W, gp);
   Inst& in = w->in[i - 1];
-  if (in.log_len + n_adm > g.A) log_pass(w, g, i, 0, 0, w->now);
+  if (in.log_len + n_adm > g.A) log_pass(w, gp, i, 0, 0, w->now);
   const int log0 = in.log_len, lvl = in.level, thr = in.thr;
   const double now = w->now;
   int started = 0;
@@ -1485,7 +1520,7 @@ EC_COLD3 void start_admitted(W* w, const GP& g, int i, int head0, int n_adm, lon
         t_next = nb;
         set_event_at(g, a, slot, i, EV_ISSUE, nb, seq0 + j);
       } else {
-        double dur = svc_time(w, g, turn0 + steps, lvl, 0, thr);
+        double dur = svc_time(w, gp, turn0 + steps, lvl, 0, thr);
         t_next = now + dur;
         g.H[a].anchor = now;
         g.H[a].rem = 1.0;
