@@ -299,7 +299,7 @@ template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int LMAX>
 /* min blocks per SM: 4-warp teams 4 per SM; single-warp teams 16 per SM,
  * i.e. <= 128 registers, so that 14 of them fit next to their shared memory
  * (C3's 2,048 scenarios in one wave of 148 x 14) */
-__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 128 ? 4 : 1))
+__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 64 ? 8 : (NT <= 128 ? 4 : 1)))
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are
@@ -496,6 +496,10 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
     if (solo) return launch_engine<16, 40, 20, 20, 32>(d_scen, n_scen, traces, tables, out, ws, st);
     /* every scenario with exactly 16 instances (the Monte-Carlo sweep): the
      * count is a compile-time constant */
+#ifdef ASB_EXP_C5_NT /* experiment: another team shape for the 16-instance sweep */
+    if (fixed_m && max_instances == 16)
+      return launch_engine<-16, ASB_EXP_C5_RC, ASB_EXP_C5_DC, ASB_EXP_C5_RC - ASB_EXP_C5_DC, ASB_EXP_C5_NT>(d_scen, n_scen, traces, tables, out, ws, st);
+#endif
     if (fixed_m && max_instances == 16 && !getenv("ASB_NO_FIXED_M")) return launch_engine<-16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
     return launch_engine<16, 192, 128, 64, 128>(d_scen, n_scen, traces, tables, out, ws, st);
   }
