@@ -47,7 +47,10 @@ def main():
     res["start_spread_ms"] = float((t0.max() - t0.min()) / 1e6)
     print(json.dumps(res, indent=1))
     if len(sys.argv) > 2:
-        json.dump({**res, "sm": sm.tolist(), "dur": dur.tolist(), "ticks": ticks.tolist()}, open(sys.argv[2], "w"))
+        turns = ctr[:, _abi.CTR["turns"]].astype(np.float64)
+        json.dump({**res, "sm": sm.tolist(), "dur": dur.tolist(), "ticks": ticks.tolist(), "turns": turns.tolist(),
+                   "t0_ms": ((t0 - t0.min()) / 1e6).tolist(), "t1_ms": ((t1 - t0.min()) / 1e6).tolist()},
+                  open(sys.argv[2], "w"))
 
 
 if __name__ == "__main__":
