@@ -68,14 +68,14 @@ def run_oracle(batch, decisions: bool = True, turn_log: bool = True, threads: in
 
 
 def run_host_engine(batch, small_buffers: bool = False, decisions: bool = True, turn_log: bool = True,
-                    timeseries: bool = False):
+                    timeseries: bool = False, serial_due: bool = False):
     """1-lane CPU build of the GPU engine core (test harness); returns (outputs, stats)."""
     lib = _load(_build.build_host_engine(), "host_engine_run", [C.c_int32])
     olib = _load(_build.build_oracle(), "oracle_run_scenarios", [C.c_int32])
     arrays = alloc_host_outputs(batch, decisions, turn_log, timeseries)
     tp, tb, out = _structs(batch, arrays)
     scen = np.ascontiguousarray(batch.scen)
-    lib.host_engine_run(scen.ctypes.data, batch.n, C.byref(tp), C.byref(tb), C.byref(out), int(small_buffers))
+    lib.host_engine_run(scen.ctypes.data, batch.n, C.byref(tp), C.byref(tb), C.byref(out), int(small_buffers) | (2 if serial_due else 0))
     stats = np.zeros(batch.n, dtype=_abi.STATS_DTYPE)
     olib.oracle_scenario_stats(scen.ctypes.data, batch.n, C.byref(out), stats.ctypes.data)
     return arrays, stats

@@ -299,7 +299,10 @@ template <int MAXM, int RCAP, int DCAP, int ACAP, int NT, int LMAX>
 /* min blocks per SM: 4-warp teams 4 per SM; single-warp teams 16 per SM,
  * i.e. <= 128 registers, so that 14 of them fit next to their shared memory
  * (C3's 2,048 scenarios in one wave of 148 x 14) */
-__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 64 ? 8 : (NT <= 128 ? 4 : 1)))
+#ifndef EC_QUAD_MINB
+#define EC_QUAD_MINB 4 /* 4-warp teams per SM the register budget is cut for */
+#endif
+__global__ void __launch_bounds__(NT, NT <= 32 ? 16 : (NT <= 64 ? 8 : (NT <= 128 ? EC_QUAD_MINB : 1)))
     asb_engine_kernel(const AsbScenario* __restrict__ scen, int n_scen, AsbTracePool tp, AsbTablePool tb,
                       AsbOutputs out, Workspace ws) {
   /* one CTA = one scenario team: warp 0 runs the engine, warps 1.. are

@@ -3379,6 +3379,101 @@ EC_COLD2 bool serial_step(W* w, const GP& g, double win_end) {
   return true;
 }
 
+/* Single-warp teams, windows with a handful of due agents (C3 averages 2.7
+ * records per batch): the exact serial event loop over the window's due
+ * list instead of speculate / sort / walk / apply.  The list holds every
+ * agent with an event left in the window (the tick sweep and the epoch
+ * collected them; agents the handlers re-time are appended as it runs,
+ * cand_collect), so the next event is the minimum over the list and the
+ * next arrival — serial_step's argmin without its sweep over every alive
+ * slot.  A list that outgrows DCAP hands the rest of the window back to the
+ * batches (due_ready = 0: they re-collect from the slots).
+ * Measured slower on C3 and therefore OFF (EC_SERIAL_DUE_MAX = 0; an
+ * experiment knob, exact either way — tests/test_host_engine.py runs it):
+ * 342 ms with lists of <= 8, 328 ms with <= 20, 414 ms with <= 3, against
+ * 310 ms for the batches.  One serial handler costs more than a whole
+ * batch's share per record, and mixing both paths doubles the hot code. */
+#ifndef EC_SERIAL_DUE_MAX
+#define EC_SERIAL_DUE_MAX 0
+#endif
+#ifndef EC_SERIAL_DUE_ON /* which teams take the serial path (the 1-lane host harness switches it at run time) */
+#define EC_SERIAL_DUE_ON(W) (W::NT == 32)
+#endif
+template <class W, int DCAP>
+EC_COLD3 int serial_due(W* w, const GP& g, double win_end) {
+  EC_LANE0 w->cand_collect = 1;
+  t_sync();
+  int rc = BATCH_DONE;
+  for (;;) {
+    const int nd = w->n_cand;
+    if (nd > DCAP) {
+      rc = BATCH_MORE;
+      break;
+    }
+    unsigned long long bt = EC_INF_BITS;
+    unsigned bp = 0xffffffffu;
+    long long bs = 0x7fffffffffffffffll;
+    int ba = -1;
+    for (int j = EC_LANE; j < nd; j += EC_TSIZE) {
+      const int a = w->due[j];
+      const int pr = g.H[a].next_prio;
+      if (pr <= 0) continue; /* a candidate no longer due */
+      const unsigned long long tb = ec_bits(g.H[a].next_t);
+      const long long s = g.H[a].next_seq;
+      if (key_less(tb, (unsigned)pr, bt, bp) || (tb == bt && (unsigned)pr == bp && s < bs)) {
+        bt = tb;
+        bp = (unsigned)pr;
+        bs = s;
+        ba = a;
+      }
+    }
+    for (int off = EC_TSIZE / 2; off > 0; off >>= 1) {
+      unsigned long long ot = t_shfl_xor_ull(bt, off);
+      unsigned op = (unsigned)t_shfl_xor_i((int)bp, off);
+      long long os = t_shfl_xor_ll(bs, off);
+      int oa = t_shfl_xor_i(ba, off);
+      if (key_less(ot, op, bt, bp) || (ot == bt && op == bp && os < bs)) {
+        bt = ot;
+        bp = op;
+        bs = os;
+        ba = oa;
+      }
+    }
+    /* the next arrival competes at priority 4 (as in serial_step) */
+    int arr = -1;
+    if (w->arr_ptr < g.A) {
+      const int a = g.arr_order[w->arr_ptr];
+      const double t = g.arrival[a];
+      if (t < w->sc.sim_duration && key_less(ec_bits(t), EV_ARRIVAL, bt, bp)) arr = a;
+    }
+    t_sync(); /* every lane has read arr_ptr and the list before lane 0 commits */
+    if (arr < 0 && ba < 0) break;
+    const double t = arr >= 0 ? g.arrival[arr] : ec_from_bits(bt);
+    if (!(w->incl ? t <= win_end : t < win_end)) break;
+    if (arr >= 0) {
+      EC_LANE0 {
+        w->now = t;
+        const int target = route_arrival(w);
+        commit_arrival(w, g, arr, target, w->arr_ptr);
+      }
+      t_sync();
+      continue;
+    }
+    Rec r;
+    r.t = t;
+    r.prio = (short)bp;
+    r.agent = ba;
+    r.inst = g.H[ba].inst;
+    exec_serial(w, g, r);
+  }
+  EC_LANE0 {
+    w->cand_collect = 0;
+    w->due_ready = 0;
+  }
+  t_sync();
+  return rc;
+}
+
 /* TS: the scenario writes timeseries rows (g.ts_rows) and runs the exact
  * serial loop; a separate instantiation keeps the batched engine's code
  * unchanged */
@@ -3465,7 +3560,11 @@ EC_DEV void run_scenario(W* w, const GP& g) {
         }
         continue;
       }
-      int rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);
+      int rc;
+      if (EC_SERIAL_DUE_ON(W) && EC_SERIAL_DUE_MAX > 0 && w->due_ready && w->n_cand <= EC_SERIAL_DUE_MAX)
+        rc = serial_due<W, DCAP>(w, g, win_end);
+      else
+        rc = batch<W, RCAP, DCAP, ACAP>(w, g, win_end);
       if (rc == BATCH_MORE) continue;
       if (rc == BATCH_DONE) break;
       /* a same-timestamp burst larger than the due buffer: one exact step */

@@ -60,6 +60,11 @@ static inline int t_atomic_min_i(int* p, int v) { int o = *p; if (v < o) *p = v;
 static inline unsigned long long t_warp_min_ull(unsigned long long v) { return v; }
 static inline void t_warp_min_key(unsigned long long&, unsigned&) {}
 
+/* the small-window serial loop (single-warp GPU teams) on demand */
+static int host_serial_due = 0;
+#define EC_SERIAL_DUE_ON(W) (host_serial_due != 0)
+#define EC_SERIAL_DUE_MAX 8 /* off in the GPU build (measured slower); an exact alternative here */
+
 #include "../../paper_2604_16682_b200/csrc/engine_core.h"
 
 /* small buffers on purpose: exercises the overflow / horizon / bisection paths */
@@ -150,6 +155,8 @@ static int run_all(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* 
 
 extern "C" int host_engine_run(const AsbScenario* scen, int32_t n_scen, const AsbTracePool* tp,
                                const AsbTablePool* tb, const AsbOutputs* out, int32_t small_buffers) {
-  if (small_buffers) return run_all<16, 8, 4>(scen, n_scen, tp, tb, out);
+  /* bit 0: small buffers; bit 1: the small-window serial loop */
+  host_serial_due = (small_buffers & 2) != 0;
+  if (small_buffers & 1) return run_all<16, 8, 4>(scen, n_scen, tp, tb, out);
   return run_all<256, 128, 64>(scen, n_scen, tp, tb, out);
 }

@@ -84,3 +84,15 @@ def test_host_engine_c5_scenario():
     want, _ = run_oracle(batch, decisions=False)
     got, _ = run_host_engine(batch, decisions=False)
     assert array_outputs_equal(want, got) is None
+
+
+@pytest.mark.parametrize("small", [False, True])
+def test_host_engine_serial_due_windows(small):
+    """The single-warp teams' small-window serial loop (serial_due: the exact
+    event loop over the window's due list, batches when the list outgrows
+    the buffer) against the oracle, on the goldens and random configs."""
+    for batch in (golden_batch(CASES), prepare_batch(random_configs(3, 24))):
+        want, _ = run_oracle(batch)
+        got, _ = run_host_engine(batch, small_buffers=small, serial_due=True)
+        diff = array_outputs_equal(want, got)
+        assert diff is None, (small, diff)
