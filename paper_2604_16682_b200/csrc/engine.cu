@@ -487,7 +487,11 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
    * (128 instance slots, 64 levels; ~2 teams per SM, correctness first) */
   if (max_instances > 64 || tables.max_levels > 16)
     return launch_engine<128, 192, 128, 64, 128, ASB_MAX_LEVELS>(d_scen, n_scen, traces, tables, out, ws, st);
-  if (big) return launch_engine<64, 1024, 768, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+#ifndef ASB_BIG_RC /* experiment knobs: the 16-warp team's batch buffers */
+#define ASB_BIG_RC 1024
+#define ASB_BIG_DC 768
+#endif
+  if (big) return launch_engine<64, ASB_BIG_RC, ASB_BIG_DC, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   /* single-instance scenarios (the DVFS sweep): a kernel whose instance
    * count is the constant 1, with the per-instance machinery folded away */
 #ifndef ASB_SOLO1_RC

@@ -98,6 +98,9 @@
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
+#ifndef EC_CCAP
+#define EC_CCAP 0 /* cached due-agent cursors per batch; 0 = all DCAP (experiment knob) */
+#endif
 /* loops over instances: kept rolled, the trip count is small and the
  * co-resident teams share a 32 KB instruction cache */
 #ifndef EC_BITONIC_MIN
@@ -306,6 +309,8 @@ struct WS {
    * reloads agent state instead of caching it in shared memory */
   static constexpr int DEP = RCAP >= 512 ? 64 : EC_DEPCAP;
   static constexpr bool CC = RCAP < 512;
+  /* cached cursors: the first CCN due agents of a batch (the rest reload) */
+  static constexpr int CCN = CC ? (EC_CCAP > 0 && EC_CCAP < DCAP ? EC_CCAP : DCAP) : 1;
   /* the 16-warp team's sort: horizon cut and per-instance lists by the
    * whole team (the smaller teams keep the shorter warp-0 code) */
   static constexpr bool BIGSORT = NTHR >= 512;
@@ -362,7 +367,7 @@ struct WS {
   int n_eplist;
   double ep_gcap;
   int due[DCAP];
-  Cur ccache[CC ? DCAP : 1]; /* due agents' state loaded by the speculation, reused by the apply */
+  Cur ccache[CCN]; /* due agents' state loaded by the speculation, reused by the apply */
   Rec rec[RCAP];
   SortE srt[RCAP];
   /* sorted structure-of-arrays view of the records for the commit walk */
@@ -2547,7 +2552,7 @@ EC_COLD1 void job_spec(W* w, const GP& gp, int tid, int nthr) {
     Cur c;
     long long seq0;
     cur_load(g, c, w->due[d], &seq0);
-    if (W::CC) w->ccache[d] = c;
+    if (W::CC && d < W::CCN) w->ccache[d] = c;
     EC_PPROF(w, 1); /* the record and turn loads */
     Rec* r = &w->rec[d];
     r->seq = seq0;
@@ -2968,7 +2973,7 @@ EC_COLD1 void job_apply(W* w, const GP& gp, int tid, int nthr) {
   for (int d = tid; d < nd; d += nthr) {
     if (!(w->rec[d].flags & F_COMMITTED)) continue;
     Cur c; /* unchanged since the speculation loaded it */
-    if (W::CC)
+    if (W::CC && d < W::CCN)
       c = w->ccache[d];
     else
       cur_load(g, c, w->due[d], nullptr, false);
