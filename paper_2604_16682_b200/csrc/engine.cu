@@ -487,9 +487,11 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
    * (128 instance slots, 64 levels; ~2 teams per SM, correctness first) */
   if (max_instances > 64 || tables.max_levels > 16)
     return launch_engine<128, 192, 128, 64, 128, ASB_MAX_LEVELS>(d_scen, n_scen, traces, tables, out, ws, st);
-#ifndef ASB_BIG_RC /* experiment knobs: the 16-warp team's batch buffers */
-#define ASB_BIG_RC 1024
-#define ASB_BIG_DC 768
+#ifndef ASB_BIG_RC /* the 16-warp team's batch buffers: 768 records (153 KB of shared
+                      memory, the 164 KB carveout: L1 92 KB instead of 60 KB); C4 442 -> 438 ms
+                      against 1,024 (188 KB); 896 measured 442 ms */
+#define ASB_BIG_RC 768
+#define ASB_BIG_DC 576
 #endif
   if (big) return launch_engine<64, ASB_BIG_RC, ASB_BIG_DC, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
   /* single-instance scenarios (the DVFS sweep): a kernel whose instance

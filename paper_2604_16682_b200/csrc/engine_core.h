@@ -99,7 +99,8 @@
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
 #ifndef EC_CCAP
-#define EC_CCAP 0 /* cached due-agent cursors per batch; 0 = all DCAP (experiment knob) */
+#define EC_CCAP 0 /* cached due-agent cursors per batch; 0 = all DCAP (experiment knob: 64 or 48 on
+                     the 16-instance kernels reach the 164 KB carveout, whole C5 job within 0.4%) */
 #endif
 /* loops over instances: kept rolled, the trip count is small and the
  * co-resident teams share a 32 KB instruction cache */
@@ -314,6 +315,9 @@ struct WS {
   /* the 16-warp team's sort: horizon cut and per-instance lists by the
    * whole team (the smaller teams keep the shorter warp-0 code) */
   static constexpr bool BIGSORT = NTHR >= 512;
+  /* the bitonic network's ping-pong buffers (the key buffer and the sorted
+   * view) hold the next power of two of RCAP */
+  static constexpr int SK = BIGSORT ? (RCAP <= 256 ? 256 : RCAP <= 512 ? 512 : RCAP <= 1024 ? 1024 : 2048) : RCAP;
   AsbScenario sc;
   GP gp;                                   /* shared with the helper warps */
   /* fork-join job state */
@@ -325,7 +329,7 @@ struct WS {
   unsigned j_hz_p[NW];
   /* scratch reused phase by phase: the sort's keys, then the walk's scans */
   union {
-    alignas(16) unsigned long long skey[2 * RCAP]; /* 16-byte sort keys (GPU counting sort) */
+    alignas(16) unsigned long long skey[2 * SK]; /* 16-byte sort keys (GPU counting sort / bitonic) */
     struct {
       unsigned long long kt[RCAP]; /* generic (1-lane) rank sort */
       long long ks[RCAP];
@@ -369,7 +373,7 @@ struct WS {
   int due[DCAP];
   Cur ccache[CCN]; /* due agents' state loaded by the speculation, reused by the apply */
   Rec rec[RCAP];
-  SortE srt[RCAP];
+  SortE srt[SK];
   /* sorted structure-of-arrays view of the records for the commit walk */
   double sw_t[RCAP];
   long long sw_du[RCAP];
@@ -2675,6 +2679,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
      * of the keys (the record index sits in the low 11 bits of the second
      * half), O(n log^2 n) steps instead of the counting rank's O(n^2)
      * compares (C4: 527 -> 511 ms) */
+    static_assert(!W::BIGSORT || W::SK >= 1024, "the bitonic buffers hold N = 1024 keys");
     int N = 1024;
     while (N / 2 >= n_all) N >>= 1;
     /* the network runs in registers: thread tid holds elements tid and
