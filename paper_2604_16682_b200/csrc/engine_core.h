@@ -98,6 +98,10 @@
 #ifndef EC_DEPCAP
 #define EC_DEPCAP 16 /* arrivals + reassignment checks per parallel walk (small teams) */
 #endif
+#ifndef EC_TEAMSORT_MIN_NT
+#define EC_TEAMSORT_MIN_NT 512 /* teams of at least this many threads build the sort's horizon cut and
+                                  per-instance lists with the whole team (smaller: warp 0; experiment knob) */
+#endif
 #ifndef EC_CCAP
 #define EC_CCAP 0 /* cached due-agent cursors per batch; 0 = all DCAP (experiment knob: 64 or 48 on
                      the 16-instance kernels reach the 164 KB carveout, whole C5 job within 0.4%) */
@@ -314,10 +318,10 @@ struct WS {
   static constexpr int CCN = CC ? (EC_CCAP > 0 && EC_CCAP < DCAP ? EC_CCAP : DCAP) : 1;
   /* the 16-warp team's sort: horizon cut and per-instance lists by the
    * whole team (the smaller teams keep the shorter warp-0 code) */
-  static constexpr bool BIGSORT = NTHR >= 512;
+  static constexpr bool BIGSORT = NTHR >= EC_TEAMSORT_MIN_NT;
   /* the bitonic network's ping-pong buffers (the key buffer and the sorted
    * view) hold the next power of two of RCAP */
-  static constexpr int SK = BIGSORT ? (RCAP <= 256 ? 256 : RCAP <= 512 ? 512 : RCAP <= 1024 ? 1024 : 2048) : RCAP;
+  static constexpr int SK = NTHR >= 512 ? (RCAP <= 256 ? 256 : RCAP <= 512 ? 512 : RCAP <= 1024 ? 1024 : 2048) : RCAP;
   AsbScenario sc;
   GP gp;                                   /* shared with the helper warps */
   /* fork-join job state */
@@ -2679,7 +2683,7 @@ EC_COLD1 void job_sort(W* w, const GP& g, int tid, int nthr) {
      * of the keys (the record index sits in the low 11 bits of the second
      * half), O(n log^2 n) steps instead of the counting rank's O(n^2)
      * compares (C4: 527 -> 511 ms) */
-    static_assert(!W::BIGSORT || W::SK >= 1024, "the bitonic buffers hold N = 1024 keys");
+    static_assert(W::NT < 512 || W::SK >= 1024, "the bitonic buffers hold N = 1024 keys");
     int N = 1024;
     while (N / 2 >= n_all) N >>= 1;
     /* the network runs in registers: thread tid holds elements tid and
