@@ -43,7 +43,11 @@
 #define EC_COLD4 __device__ __noinline__
 #define EC_LANE ((int)(threadIdx.x & 31))
 #ifndef ASB_NO_PREFETCH
+#ifdef ASB_PREFETCH_L1 /* experiment: the due agents' lines into the SM's L1 instead of L2 */
+#define EC_PREFETCH_L2(p) asm volatile("prefetch.global.L1 [%0];" ::"l"(p))
+#else
 #define EC_PREFETCH_L2(p) asm volatile("prefetch.global.L2 [%0];" ::"l"(p))
+#endif
 #endif
 #define EC_TSIZE 32
 #define EC_NAN __longlong_as_double(0x7ff8000000000000ll)
