@@ -497,7 +497,13 @@ int asb_run_scenarios(const AsbScenario* d_scen, int32_t n_scen, int32_t max_ins
 #define ASB_BIG_RC 768
 #define ASB_BIG_DC 576
 #endif
-  if (big) return launch_engine<64, ASB_BIG_RC, ASB_BIG_DC, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+  if (big) {
+    /* every scenario with exactly 64 instances (the thrashing regime C4): the
+     * count is a compile-time constant, as for the 16-instance sweep */
+    if (fixed_m && max_instances == 64 && !getenv("ASB_NO_FIXED_M"))
+      return launch_engine<-64, ASB_BIG_RC, ASB_BIG_DC, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+    return launch_engine<64, ASB_BIG_RC, ASB_BIG_DC, 128, 512>(d_scen, n_scen, traces, tables, out, ws, st);
+  }
   /* single-instance scenarios (the DVFS sweep): a kernel whose instance
    * count is the constant 1, with the per-instance machinery folded away */
 #ifndef ASB_SOLO1_RC
